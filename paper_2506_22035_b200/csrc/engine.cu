@@ -1,0 +1,1115 @@
+// sm_100a SPIDER stencil engine: strided-swapped 2:4 kernel rows on the
+// Blackwell sparse tensor cores (tcgen05.mma.sp), plus the support kernels
+// behind the C ABI (include/spider.h).
+//
+// One launch = one Jacobi step (pipeline.py:247-261 / core.py:176-181) over a
+// tile range.  Persistent, warp-specialised CTA (one per SM):
+//   warps 0-3  epilogue : TMEM -> registers -> fp16 -> quad/octet transpose ->
+//                         coalesced 16-byte global stores
+//   warps 4-11 producer : LDG.128 of the natural input rows -> warp shuffles
+//                         -> PRMT byte permutes that apply the reference's
+//                         input-row involution (transform.py:130-139) and the
+//                         2L-window expansion (pipeline.py:176-186, 251-252)
+//                         -> STS.128 straight into the UMMA K-major B image.
+//                         The swap costs no extra pass: it is folded into the
+//                         register->smem write.
+//   warp 12    MMA      : one thread issues S tcgen05.mma.sp per tile with the
+//                         compressed kernel (A) and metadata (E) resident in
+//                         TMEM for the whole launch.
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "spider_internal.h"
+
+namespace spd {
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE%=;\nbra WAIT%=;\nDONE%=:\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_NONE (verified layout, see
+// tools/umma_sp_probe.cu): core matrix = 8 rows x 16 B, LBO = stride between
+// K-adjacent core matrices, SBO = stride between 8-row groups.
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100)
+  return d;
+}
+
+// Instruction descriptor for kind::f16 sparse, fp32 accumulate, K-major A/B.
+__host__ __device__ constexpr uint32_t idesc_sparse_f16(int m, int n, bool bf16) {
+  return (1u << 2)                        // sparse
+         | (1u << 4)                      // D = f32
+         | ((bf16 ? 1u : 0u) << 7)        // A format
+         | ((bf16 ? 1u : 0u) << 10)       // B format
+         | ((uint32_t)(n >> 3) << 17)     // N
+         | ((uint32_t)(m >> 4) << 24);    // M
+}
+
+// D[tmem] (+)= A[tmem] * B[smem desc] with metadata E[tmem]  (ts form)
+__device__ __forceinline__ void mma_sp_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t e,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%3], %5, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(e), "r"(accum), "r"(idesc));
+}
+
+__device__ __forceinline__ void tmem_st_x1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v));
+}
+
+__device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                       uint32_t d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+
+template <typename T>
+struct Cvt;
+template <>
+struct Cvt<__half> {
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+template <>
+struct Cvt<__nv_bfloat16> {
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Compile-time permutation tables
+
+// input_row_permutation (transform.py:130-139): slot q of the swapped window
+// holds window element PI(q).
+__host__ __device__ constexpr int perm_slot(int L, int parity, int q) {
+  return (q < L) ? (((q % 2) == parity) ? q + L : q) : ((((q - L) % 2) == parity) ? q - L : q);
+}
+
+// __byte_perm selector that packs half `ha` of word x (low) and half `hb` of
+// word y (high).
+__host__ __device__ constexpr uint32_t sel_halves(int ha, int hb) {
+  return (uint32_t)((2 * ha) | ((2 * ha + 1) << 4) | ((4 + 2 * hb) << 8) | ((5 + 2 * hb) << 12));
+}
+
+// ---------------------------------------------------------------------------
+// Kernel parameters
+
+struct StepParams {
+  Geometry g;
+  const void* in;
+  void* out;
+  int64_t pitch, plane, origin;
+  int64_t nx;                // x extent (interior)
+  int64_t row_lo, row_hi;    // valid output rows (2D: y, 3D: z, 1D: unused)
+  int64_t ny;                // 3D: y extent (rows beyond it are masked)
+  int tiles_x, tiles_y, tiles_z;
+  int tile_y0, tile_z0;      // first tile row / plane of the range
+  int n_tiles;
+  const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
+  const uint32_t* e_words;   // [S][128]
+};
+
+constexpr int kEpiWarps = 4;
+constexpr int kProdWarps = 8;
+constexpr int kThreads = 32 * (kEpiWarps + kProdWarps + 1);
+constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+
+template <int L, int NTILE, int NSTAGE, int NACC, int NQ>
+struct Cfg {
+  static constexpr int KC = 2 * L / 8;
+  static constexpr int CPL = 8 / L;          // chunks per lane per 16-B load
+  static constexpr int SEG = 32 * CPL;       // chunks per warp segment
+  static constexpr int SEGS = NTILE / SEG;   // segments per tile row
+  static constexpr int ACC_COL = 0;
+  static constexpr int E_COL = NACC * NTILE;
+  // E for MMA s at E_COL + 2s: bit 0 of the metadata TMEM address is the
+  // sparse_id2 selector, so each MMA's column must be even (odd -> misaligned).
+  static constexpr int A_COL = E_COL + 2 * SPD_MAX_S;
+  static constexpr int TMEM_COLS = 512;  // host checks A_COL + 8*S <= 512
+  static_assert(NTILE % SEG == 0, "tile width must be whole warp segments");
+};
+
+
+
+// ---------------------------------------------------------------------------
+// The stencil step kernel.
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NACC, int NQ>
+__global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
+  using C = Cfg<L, NTILE, NSTAGE, NACC, NQ>;
+  constexpr int KC = C::KC;
+  const Geometry& g = p.g;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int sbo = g.b_sbo;
+  const int stage_bytes = (NTILE / 8) * sbo;
+  uint8_t* bimg = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * stage_bytes);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC);
+  const uint32_t bimg_s = smem_u32(bimg);
+  const uint32_t bar_full = smem_u32(bars);
+  const uint32_t bar_empty = bar_full + 8 * NSTAGE;
+  const uint32_t bar_accf = bar_full + 16 * NSTAGE;
+  const uint32_t bar_acce = bar_accf + 8 * NACC;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(bar_full + 8 * s, kProdWarps);
+      mbar_init(bar_empty + 8 * s, 1);
+    }
+    for (int a = 0; a < NACC; ++a) {
+      mbar_init(bar_accf + 8 * a, 1);
+      mbar_init(bar_acce + 8 * a, kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_holder)),
+                 "n"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  // Resident operands: E words and compressed A into TMEM (loaded once per
+  // launch; the stencil kernel is constant — the B200 analogue of keeping the
+  // kernel matrix in registers).
+  if (warp < kEpiWarps) {
+    const int m = warp * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int s = 0; s < g.s; ++s) {
+      tmem_st_x1(lane_base + C::E_COL + 2 * s, __ldg(p.e_words + s * 128 + m));
+      const uint4* src = reinterpret_cast<const uint4*>(p.a_img + ((size_t)s * 128 + m) * 16);
+      uint4 a0 = __ldg(src), a1 = __ldg(src + 1);
+      uint32_t col = lane_base + C::A_COL + 8 * s;
+      tmem_st_x1(col + 0, a0.x);
+      tmem_st_x1(col + 1, a0.y);
+      tmem_st_x1(col + 2, a0.z);
+      tmem_st_x1(col + 3, a0.w);
+      tmem_st_x1(col + 4, a1.x);
+      tmem_st_x1(col + 5, a1.y);
+      tmem_st_x1(col + 6, a1.z);
+      tmem_st_x1(col + 7, a1.w);
+    }
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  const T* __restrict__ in = static_cast<const T*>(p.in);
+  T* __restrict__ out = static_cast<T*>(p.out);
+
+  auto tile_origin = [&](int t, int64_t& z0, int64_t& y0, int64_t& x0) {
+    int bx = t % p.tiles_x;
+    int rest = t / p.tiles_x;
+    int by = rest % p.tiles_y;
+    int bz = rest / p.tiles_y;
+    x0 = (int64_t)bx * g.tile_x;
+    y0 = (int64_t)(p.tile_y0 + by) * g.tile_y;
+    z0 = (int64_t)(p.tile_z0 + bz) * g.tile_z;
+  };
+
+  if (warp >= kEpiWarps && warp < kMmaWarp) {
+    // ===================== producer: natural rows -> permuted B image =====
+    const int pw = warp - kEpiWarps;
+    const int n_items = g.r_in * C::SEGS;
+    int it = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+      const int stage = it % NSTAGE;
+      const uint32_t sphase = (it / NSTAGE) & 1;
+      int64_t z0, y0, x0;
+      tile_origin(t, z0, y0, x0);
+      uint4 cur[NQ], edge[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int item = pw + q * kProdWarps;
+        if (item < n_items) {
+          const int b = item / C::SEGS, sg = item % C::SEGS;
+          const T* row = in + p.origin + (z0 + g.in_dz[b]) * p.plane + (y0 + g.in_dy[b]) * p.pitch +
+                         x0 + g.in_dx[b] + (int64_t)sg * 256;
+          cur[q] = __ldg(reinterpret_cast<const uint4*>(row) + lane);
+          if (lane == 0) edge[q] = __ldg(reinterpret_cast<const uint4*>(row) - 1);
+          if (lane == 31) edge[q] = __ldg(reinterpret_cast<const uint4*>(row) + 32);
+        }
+      }
+      mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+      const uint32_t sbase = bimg_s + stage * stage_bytes;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int item = pw + q * kProdWarps;
+        if (item < n_items) {
+          const int b = item / C::SEGS, sg = item % C::SEGS;
+          uint32_t ext[12];
+          ext[4] = cur[q].x;
+          ext[5] = cur[q].y;
+          ext[6] = cur[q].z;
+          ext[7] = cur[q].w;
+          ext[0] = __shfl_up_sync(0xffffffffu, cur[q].x, 1);
+          ext[1] = __shfl_up_sync(0xffffffffu, cur[q].y, 1);
+          ext[2] = __shfl_up_sync(0xffffffffu, cur[q].z, 1);
+          ext[3] = __shfl_up_sync(0xffffffffu, cur[q].w, 1);
+          ext[8] = __shfl_down_sync(0xffffffffu, cur[q].x, 1);
+          ext[9] = __shfl_down_sync(0xffffffffu, cur[q].y, 1);
+          ext[10] = __shfl_down_sync(0xffffffffu, cur[q].z, 1);
+          ext[11] = __shfl_down_sync(0xffffffffu, cur[q].w, 1);
+          if (lane == 0) {
+            ext[0] = edge[q].x;
+            ext[1] = edge[q].y;
+            ext[2] = edge[q].z;
+            ext[3] = edge[q].w;
+          }
+          if (lane == 31) {
+            ext[8] = edge[q].x;
+            ext[9] = edge[q].y;
+            ext[10] = edge[q].z;
+            ext[11] = edge[q].w;
+          }
+          uint32_t w[C::CPL][KC][4];
+#pragma unroll
+          for (int c = 0; c < C::CPL; ++c)
+#pragma unroll
+            for (int kc = 0; kc < KC; ++kc)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                // element index in ext (16-bit units): x = 8*lane - 8 + e
+                constexpr int R = (L - 2) / 2;
+                const int e0 = 8 + c * L - R + perm_slot(L, PARITY, 8 * kc + 2 * u);
+                const int e1 = 8 + c * L - R + perm_slot(L, PARITY, 8 * kc + 2 * u + 1);
+                w[c][kc][u] = __byte_perm(ext[e0 / 2], ext[e1 / 2], sel_halves(e0 % 2, e1 % 2));
+              }
+          const int n0 = sg * C::SEG + lane * C::CPL;  // first chunk of this lane
+          if (C::CPL == 2) {
+            // Lanes 4-7 of each quarter-warp write the next core-matrix group at
+            // the same bank offsets as lanes 0-3: store their odd chunk first so
+            // every STS.128 phase covers all 32 banks once.
+            const bool flip = (lane >> 2) & 1;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int n = n0 + (c ^ (int)flip);
+              const uint32_t gbase = sbase + (n / 8) * sbo + (n % 8) * 16 + b * KC * 128;
+#pragma unroll
+              for (int kc = 0; kc < KC; ++kc) {
+                const int ci = c ^ (int)flip;
+                uint32_t a0 = ci ? w[C::CPL - 1][kc][0] : w[0][kc][0];
+                uint32_t a1 = ci ? w[C::CPL - 1][kc][1] : w[0][kc][1];
+                uint32_t a2 = ci ? w[C::CPL - 1][kc][2] : w[0][kc][2];
+                uint32_t a3 = ci ? w[C::CPL - 1][kc][3] : w[0][kc][3];
+                sts_v4(gbase + kc * 128, a0, a1, a2, a3);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < C::CPL; ++c) {
+              const int n = n0 + c;
+              const uint32_t gbase = sbase + (n / 8) * sbo + (n % 8) * 16 + b * KC * 128;
+#pragma unroll
+              for (int kc = 0; kc < KC; ++kc) sts_v4(gbase + kc * 128, w[c][kc][0], w[c][kc][1], w[c][kc][2], w[c][kc][3]);
+            }
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_full + 8 * stage);
+    }
+  } else if (warp == kMmaWarp) {
+    // ===================== MMA issuer ======================================
+    const uint32_t idesc = idesc_sparse_f16(128, NTILE, std::is_same<T, __nv_bfloat16>::value);
+    int it = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+      const int stage = it % NSTAGE;
+      const uint32_t sphase = (it / NSTAGE) & 1;
+      const int acc = it % NACC;
+      const uint32_t aphase = (it / NACC) & 1;
+      mbar_wait(bar_acce + 8 * acc, aphase ^ 1);
+      mbar_wait(bar_full + 8 * stage, sphase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sbase = bimg_s + stage * stage_bytes;
+        const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
+        for (int s = 0; s < g.s; ++s) {
+          const uint64_t bdesc = umma_desc(sbase + g.start_row[s] * KC * 128, 128, sbo);
+          mma_sp_ts(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
+        }
+        tc_commit(bar_empty + 8 * stage);
+        tc_commit(bar_accf + 8 * acc);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ===================== epilogue ========================================
+    const int m = warp * 32 + lane;       // TMEM lane == M row
+    const int alpha = m / L;              // output row of the tile
+    const int d = lane % L;               // position in the L-lane group
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    int it = 0;
+    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+      const int acc = it % NACC;
+      const uint32_t aphase = (it / NACC) & 1;
+      int64_t z0, y0, x0;
+      tile_origin(t, z0, y0, x0);
+      const int64_t z = z0 + g.out_dz[alpha];
+      const int64_t y = y0 + g.out_dy[alpha];
+      const int64_t xr = x0 + g.out_dx[alpha];  // x of chunk 0 of this row
+      bool row_ok;
+      if (g.d == 3) row_ok = z >= p.row_lo && z < p.row_hi && y < p.ny;
+      else if (g.d == 2) row_ok = y >= p.row_lo && y < p.row_hi;
+      else row_ok = true;
+      const int64_t chunk_lim = (p.nx - xr) / L;  // valid chunks in this row
+      T* orow = out + p.origin + z * p.plane + y * p.pitch + xr;
+      mbar_wait(bar_accf + 8 * acc, aphase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cb = 0; cb < NTILE / 32; ++cb) {
+        uint32_t v[32];
+        tmem_ld_x32(lane_base + C::ACC_COL + acc * NTILE + cb * 32, v);
+        tmem_wait_ld();
+        if (cb == NTILE / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
+        }
+        // pack pairs of columns: pk[j] = (col 2j, col 2j+1) of my lane
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = Cvt<T>::pack(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        // xor-butterfly transpose inside the L-lane group: pk[k*L + dd] goes
+        // to lane dd; afterwards pk[k*L + s] holds source lane s's word.
+#pragma unroll
+        for (int b = 1; b < L; b <<= 1) {
+          const bool upper = (d & b) != 0;
+#pragma unroll
+          for (int k = 0; k < 16 / L; ++k) {
+#pragma unroll
+            for (int dd = 0; dd < L; ++dd) {
+              if (dd & b) continue;
+              uint32_t send = upper ? pk[k * L + dd] : pk[k * L + (dd | b)];
+              uint32_t recv = __shfl_xor_sync(0xffffffffu, send, b);
+              if (upper) pk[k * L + dd] = recv;
+              else pk[k * L + (dd | b)] = recv;
+            }
+          }
+        }
+        if (row_ok) {
+#pragma unroll
+          for (int k = 0; k < 16 / L; ++k) {
+            // this lane now owns 2L consecutive points starting at chunk c0
+            const int64_t c0 = (int64_t)cb * 32 + 2 * L * k + 2 * d;
+            uint32_t w[L];
+#pragma unroll
+            for (int tt = 0; tt < L; ++tt) {
+              const int e = 2 * tt;
+              if (e < L) w[tt] = __byte_perm(pk[k * L + e], pk[k * L + e + 1], 0x5410);
+              else w[tt] = __byte_perm(pk[k * L + e - L], pk[k * L + e - L + 1], 0x7632);
+            }
+            T* dst = orow + c0 * L;
+            if (c0 + 1 < chunk_lim) {
+#pragma unroll
+              for (int q = 0; q < L / 4; ++q)
+                *reinterpret_cast<uint4*>(dst + 8 * q) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            } else if (c0 < chunk_lim) {
+              if (L == 4) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+              else *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Support kernels
+
+template <typename T>
+__device__ __forceinline__ T from_f64(double x);
+template <>
+__device__ __forceinline__ __half from_f64<__half>(double x) { return __double2half(x); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f64<__nv_bfloat16>(double x) { return __double2bfloat16(x); }
+
+struct DenseMap {
+  int64_t nzd, nyd, nxd;  // dense extents incl. halo (nzd = 1 for 2D/1D)
+  int64_t h;
+  int d;
+};
+
+// dense natural (halo-padded) fp64 <-> device layout
+template <typename T>
+__global__ void pack_kernel(DenseMap dm, int64_t pitch, int64_t plane, int64_t origin, const double* dense, T* dev) {
+  int64_t n = dm.nzd * dm.nyd * dm.nxd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t xx = i % dm.nxd, rest = i / dm.nxd;
+    int64_t yy = rest % dm.nyd, zz = rest / dm.nyd;
+    int64_t z = dm.d == 3 ? zz - dm.h : 0;
+    int64_t o = origin + z * plane + (yy - dm.h) * pitch + (xx - dm.h);
+    dev[o] = from_f64<T>(dense[i]);
+  }
+}
+
+template <typename T>
+__global__ void unpack_kernel(DenseMap dm, int64_t pitch, int64_t plane, int64_t origin, const T* dev, double* dense) {
+  int64_t n = dm.nzd * dm.nyd * dm.nxd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t xx = i % dm.nxd, rest = i / dm.nxd;
+    int64_t yy = rest % dm.nyd, zz = rest / dm.nyd;
+    int64_t z = dm.d == 3 ? zz - dm.h : 0;
+    int64_t o = origin + z * plane + (yy - dm.h) * pitch + (xx - dm.h);
+    dense[i] = (double)static_cast<float>(dev[o]);
+  }
+}
+
+// naive_apply on device in fp64 (core.py:151-182): same row-major tap order,
+// acc = 0; acc = acc + (w * x) with separate roundings (no FMA contraction).
+__global__ void naive_f64_kernel(int d, int r, const double* __restrict__ w, int64_t nz, int64_t ny, int64_t nx,
+                                 int64_t h, const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t nxd = nx + 2 * h, nyd = (d >= 2) ? ny + 2 * h : ny + 2 * h;
+  const int64_t n = nz * ny * nx;
+  const int span = 2 * r + 1;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = i % nx, rest = i / nx;
+    int64_t y = rest % ny, z = rest / ny;
+    double acc = 0.0;
+    if (d == 3) {
+      int t = 0;
+      for (int rz = -r; rz <= r; ++rz)
+        for (int ry = -r; ry <= r; ++ry)
+          for (int rx = -r; rx <= r; ++rx, ++t) {
+            double v = in[((z + h + rz) * nyd + (y + h + ry)) * nxd + (x + h + rx)];
+            acc = __dadd_rn(acc, __dmul_rn(w[t], v));
+          }
+      out[((z + h) * nyd + (y + h)) * nxd + (x + h)] = acc;
+    } else if (d == 2) {
+      int t = 0;
+      for (int ry = -r; ry <= r; ++ry)
+        for (int rx = -r; rx <= r; ++rx, ++t) {
+          double v = in[(y + h + ry) * nxd + (x + h + rx)];
+          acc = __dadd_rn(acc, __dmul_rn(w[t], v));
+        }
+      out[(y + h) * nxd + (x + h)] = acc;
+    } else {
+      for (int t = 0; t < span; ++t) {
+        double v = in[(y + h) * nxd + (x + h + t - r)];
+        acc = __dadd_rn(acc, __dmul_rn(w[t], v));
+      }
+      out[(y + h) * nxd + (x + h)] = acc;
+    }
+  }
+}
+
+// Halo rows (2D: rows, 3D: planes) <-> contiguous message buffers.
+template <typename T>
+__global__ void halo_copy_kernel(const T* src, int64_t src_off, T* dst, int64_t dst_off, int64_t count,
+                                 int64_t run, int64_t src_stride, int64_t dst_stride) {
+  // `count` runs of `run` elements; run i at src_off + i*src_stride.
+  int64_t n = count * run;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = k / run, j = k % run;
+    dst[dst_off + i * dst_stride + j] = src[src_off + i * src_stride + j];
+  }
+}
+
+// Single sparse MMA self test: D = decode(A, E) * B, M=128, K=32, N = n.
+__global__ void mma_selftest_kernel(const uint16_t* a, const uint8_t* e, const uint16_t* b, int n, float* d) {
+  __shared__ __align__(1024) uint8_t sB[256 * 64];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int sbo = 4 * 128;
+  for (int idx = threadIdx.x; idx < 32 * n; idx += blockDim.x) {
+    int k = idx / n, c = idx % n;
+    *reinterpret_cast<uint16_t*>(sB + (c / 8) * sbo + (k / 8) * 128 + (c % 8) * 16 + (k % 8) * 2) = b[k * n + c];
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&holder)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = holder;
+  const int m = warp * 32 + lane;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  const int E_COL = 256, A_COL = 264;
+  {
+    int m0 = m % 8, k1 = (m / 8) % 2, m2 = m / 16;
+    uint32_t w = 0;
+    for (int m1 = 0; m1 < 2; ++m1)
+      for (int c4 = 0; c4 < 4; ++c4) w |= (uint32_t)(e[(m0 + 8 * m1 + 16 * m2) * 8 + 4 * k1 + c4] & 0xF) << (16 * m1 + 4 * c4);
+    tmem_st_x1(lane_base + E_COL, w);
+    for (int c = 0; c < 8; ++c) tmem_st_x1(lane_base + A_COL + c, (uint32_t)a[m * 16 + 2 * c] | ((uint32_t)a[m * 16 + 2 * c + 1] << 16));
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0 && lane == 0) {
+    mma_sp_ts(tmem, tmem + A_COL, umma_desc(smem_u32(sB), 128, sbo), tmem + E_COL, idesc_sparse_f16(128, n, false), 0u);
+    tc_commit(smem_u32(&bar));
+  }
+  __syncwarp();
+  mbar_wait(smem_u32(&bar), 0);
+  tc_fence_after();
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld_x32(lane_base + c0, v);
+    tmem_wait_ld();
+    for (int j = 0; j < 32 && c0 + j < n; ++j) d[m * n + c0 + j] = __uint_as_float(v[j]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Host side: plan, dispatch
+
+struct DevInfo {
+  int sms = 0;
+};
+
+static int cuda_err(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SPD_OK;
+  return set_error(SPD_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+}  // namespace spd
+
+struct spd_plan {
+  spd::Geometry g;
+  int d, r, parity, dtype, device, L, n_rows;
+  std::vector<double> coeffs;
+  std::vector<double> row_values;  // n_rows x L x L
+  std::vector<uint8_t> row_meta;   // n_rows x L x (L/2) x 2
+  std::vector<uint16_t> a_img;     // S x 128 x 16
+  std::vector<uint32_t> e_words;   // S x 128
+  uint16_t* d_a = nullptr;
+  uint32_t* d_e = nullptr;
+  int sms = 0;
+};
+
+namespace spd {
+
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NACC, int NQ>
+static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NACC, NQ>;
+  const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + 8 * (2 * NSTAGE + 2 * NACC) + 16;
+  static thread_local int configured_dev = -1;
+  // cudaFuncSetAttribute is per function; cheap enough to call each time on
+  // a new device, cache per thread otherwise.
+  if (configured_dev != plan->device) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
+    configured_dev = plan->device;
+  }
+  if (Cfg<L, NTILE, NSTAGE, NACC, NQ>::A_COL + 8 * plan->g.s > 512)
+    return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
+  if (sp.n_tiles <= 0) return SPD_OK;
+  int grid = sp.n_tiles < plan->sms ? sp.n_tiles : plan->sms;
+  kern<<<grid, kThreads, smem, stream>>>(sp);
+  return cuda_err(cudaGetLastError(), "spider_step_kernel launch");
+}
+
+template <typename T, int PARITY>
+static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
+  const Geometry& g = plan->g;
+  // items per producer warp: ceil(r_in * segs / 8)
+  if (g.L == 4 && g.n_tile == 128) {
+    // 2D (r_in 34, 2 segs -> 68 items) and 1D (r_in 32 -> 64 items)
+    return launch_step<T, 4, PARITY, 128, 3, 3, 9>(plan, sp, st);
+  }
+  if (g.L == 4 && g.n_tile == 64) {
+    // 3D: r_in 60, 1 seg -> 60 items
+    return launch_step<T, 4, PARITY, 64, 3, 4, 8>(plan, sp, st);
+  }
+  if (g.L == 8 && g.n_tile == 64) {
+    // 2D r=3: r_in 22, 2 segs -> 44 items; 1D: 16 rows -> 32 items
+    return launch_step<T, 8, PARITY, 64, 4, 4, 6>(plan, sp, st);
+  }
+  return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
+}
+
+static int dispatch(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
+  if (plan->dtype == SPD_DTYPE_F16)
+    return plan->parity == 0 ? dispatch_par<__half, 0>(plan, sp, st) : dispatch_par<__half, 1>(plan, sp, st);
+  return plan->parity == 0 ? dispatch_par<__nv_bfloat16, 0>(plan, sp, st)
+                           : dispatch_par<__nv_bfloat16, 1>(plan, sp, st);
+}
+
+static int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int64_t lo,
+                            int64_t hi, StepParams& sp) {
+  const Geometry& g = plan->g;
+  std::memset(&sp, 0, sizeof(sp));
+  sp.g = g;
+  sp.in = in;
+  sp.out = out;
+  sp.pitch = gd->pitch;
+  sp.plane = gd->plane;
+  sp.origin = gd->origin;
+  sp.nx = gd->nx;
+  sp.ny = gd->ny;
+  sp.a_img = plan->d_a;
+  sp.e_words = plan->d_e;
+  sp.tiles_x = (int)((gd->nx + g.tile_x - 1) / g.tile_x);
+  if (g.d == 3) {
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > gd->nz ? gd->nz : hi;
+    sp.row_lo = lo;
+    sp.row_hi = hi;
+    sp.tiles_y = (int)((gd->ny + g.tile_y - 1) / g.tile_y);
+    sp.tile_y0 = 0;
+    sp.tile_z0 = (int)(lo / g.tile_z);
+    sp.tiles_z = hi > lo ? (int)((hi + g.tile_z - 1) / g.tile_z - sp.tile_z0) : 0;
+  } else if (g.d == 2) {
+    lo = lo < 0 ? 0 : lo;
+    hi = hi > gd->ny ? gd->ny : hi;
+    sp.row_lo = lo;
+    sp.row_hi = hi;
+    sp.tiles_z = 1;
+    sp.tile_z0 = 0;
+    sp.tile_y0 = (int)(lo / g.tile_y);
+    sp.tiles_y = hi > lo ? (int)((hi + g.tile_y - 1) / g.tile_y - sp.tile_y0) : 0;
+  } else {
+    sp.row_lo = 0;
+    sp.row_hi = 1;
+    sp.tiles_y = sp.tiles_z = 1;
+  }
+  sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
+  return SPD_OK;
+}
+
+static int check_desc(const spd_plan* plan, const spd_grid_desc* gd) {
+  if (!plan || !gd) return set_error(SPD_EINVAL, "null plan or grid descriptor");
+  if (gd->nx % plan->L != 0)
+    return set_error(SPD_EINVAL, "grid width %lld must be a multiple of the x-chunk size L=%d", (long long)gd->nx,
+                     plan->L);
+  if (gd->halo < plan->r)
+    return set_error(SPD_EINVAL, "grid halo %d too small for stencil radius %d", gd->halo, plan->r);
+  return SPD_OK;
+}
+
+}  // namespace spd
+
+// ---------------------------------------------------------------------------
+// C ABI (device part)
+extern "C" {
+
+int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype, int device, spd_plan** out) {
+  using namespace spd;
+  if (!out) return set_error(SPD_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (d < 1 || d > 3) return set_error(SPD_EINVAL, "unsupported dimensionality %d", d);
+  if (parity != 0 && parity != 1) return set_error(SPD_EINVAL, "bad parity code %d", parity);
+  if (dtype != SPD_DTYPE_F16 && dtype != SPD_DTYPE_BF16) return set_error(SPD_EINVAL, "bad dtype code %d", dtype);
+  int L = band_rows(r);
+  if (L < 0) return L;
+  spd_plan* p = new spd_plan();
+  p->d = d;
+  p->r = r;
+  p->parity = parity;
+  p->dtype = dtype;
+  p->device = device;
+  p->L = L;
+  int span = 2 * r + 1;
+  int ncoef = d == 1 ? span : (d == 2 ? span * span : span * span * span);
+  p->coeffs.assign(coeffs, coeffs + ncoef);
+  p->n_rows = ncoef / span;
+  p->row_values.resize((size_t)p->n_rows * L * L);
+  p->row_meta.resize((size_t)p->n_rows * L * (L / 2) * 2);
+  for (int k = 0; k < p->n_rows; ++k) {
+    int rc = transform_row(r, parity, coeffs + (size_t)k * span, p->row_values.data() + (size_t)k * L * L,
+                           p->row_meta.data() + (size_t)k * L * L);
+    if (rc) {
+      delete p;
+      return rc;
+    }
+  }
+  int rc = build_geometry(d, r, &p->g);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  rc = pack_operands(p->g, p->n_rows, p->row_values.data(), p->row_meta.data(), dtype, p->a_img, p->e_words);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  if (device >= 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_a, p->a_img.size() * sizeof(uint16_t));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_e, p->e_words.size() * sizeof(uint32_t));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_a, p->a_img.data(), p->a_img.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->d_e, p->e_words.data(), p->e_words.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    cudaSetDevice(cur);
+    if (e != cudaSuccess) {
+      int code = cuda_err(e, "plan upload");
+      spd_plan_destroy(p);
+      return code;
+    }
+  }
+  *out = p;
+  return SPD_OK;
+}
+
+int spd_plan_destroy(spd_plan* plan) {
+  if (!plan) return SPD_OK;
+  if (plan->d_a) cudaFree(plan->d_a);
+  if (plan->d_e) cudaFree(plan->d_e);
+  delete plan;
+  return SPD_OK;
+}
+
+int spd_plan_info(const spd_plan* plan, int32_t* info) {
+  if (!plan || !info) return spd::set_error(SPD_EINVAL, "null argument");
+  const spd::Geometry& g = plan->g;
+  info[0] = g.L;
+  info[1] = g.r_in;
+  info[2] = g.r_out;
+  info[3] = g.s;
+  info[4] = g.n_tile;
+  info[5] = g.tile_z;
+  info[6] = g.tile_y;
+  info[7] = g.kc;
+  return SPD_OK;
+}
+
+int spd_plan_operands(const spd_plan* plan, uint16_t* a_img, uint32_t* e_words, int32_t* start_rows) {
+  if (!plan) return spd::set_error(SPD_EINVAL, "null plan");
+  if (a_img) std::memcpy(a_img, plan->a_img.data(), plan->a_img.size() * sizeof(uint16_t));
+  if (e_words) std::memcpy(e_words, plan->e_words.data(), plan->e_words.size() * sizeof(uint32_t));
+  if (start_rows)
+    for (int s = 0; s < plan->g.s; ++s) start_rows[s] = plan->g.start_row[s];
+  return SPD_OK;
+}
+
+int spd_plan_geometry(const spd_plan* plan, int32_t* in_off, int32_t* out_off) {
+  if (!plan) return spd::set_error(SPD_EINVAL, "null plan");
+  const spd::Geometry& g = plan->g;
+  for (int b = 0; in_off && b < g.r_in; ++b) {
+    in_off[3 * b] = g.in_dz[b];
+    in_off[3 * b + 1] = g.in_dy[b];
+    in_off[3 * b + 2] = g.in_dx[b];
+  }
+  for (int a = 0; out_off && a < g.r_out; ++a) {
+    out_off[3 * a] = g.out_dz[a];
+    out_off[3 * a + 1] = g.out_dy[a];
+    out_off[3 * a + 2] = g.out_dx[a];
+  }
+  return SPD_OK;
+}
+
+int spd_grid_layout(const spd_plan* plan, int64_t nz, int64_t ny, int64_t nx, int halo, spd_grid_desc* out) {
+  using namespace spd;
+  if (!plan || !out) return set_error(SPD_EINVAL, "null argument");
+  if (halo < plan->r) return set_error(SPD_EINVAL, "grid halo %d too small for stencil radius %d", halo, plan->r);
+  if (nx < 1 || ny < 1 || nz < 1) return set_error(SPD_EINVAL, "grid extent too small for its halo");
+  if (nx % plan->L != 0)
+    return set_error(SPD_EINVAL, "grid width %lld must be a multiple of the x-chunk size L=%d", (long long)nx,
+                     plan->L);
+  const Geometry& g = plan->g;
+  if (plan->d == 2 && nz != 1) return set_error(SPD_EINVAL, "2D grid must have nz = 1");
+  if (plan->d == 1 && (nz != 1 || ny != 1)) return set_error(SPD_EINVAL, "1D grid must have nz = ny = 1");
+  const int64_t xoff = roundup(halo > 8 ? halo : 8, 8);
+  const int64_t nx_pad = roundup(nx, g.tile_x);
+  int64_t need_x = nx_pad + 8 > nx + halo ? nx_pad + 8 : nx + halo;
+  const int64_t pitch = roundup(xoff + need_x, 64);
+  int64_t rows, planes, yoff, zoff;
+  if (plan->d == 1) {
+    rows = 2 * halo + 1;
+    yoff = halo;
+    planes = 1;
+    zoff = 0;
+  } else {
+    const int64_t ny_pad = roundup(ny, g.tile_y);
+    yoff = halo;
+    rows = halo + (ny_pad + plan->r > ny + halo ? ny_pad + plan->r : ny + halo);
+    if (plan->d == 3) {
+      const int64_t nz_pad = roundup(nz, g.tile_z);
+      zoff = halo;
+      planes = halo + (nz_pad + plan->r > nz + halo ? nz_pad + plan->r : nz + halo);
+    } else {
+      zoff = 0;
+      planes = 1;
+    }
+  }
+  out->nz = nz;
+  out->ny = ny;
+  out->nx = nx;
+  out->halo = halo;
+  out->dims = plan->d;
+  out->pitch = pitch;
+  out->plane = rows * pitch;
+  out->origin = zoff * out->plane + yoff * pitch + xoff;
+  out->alloc_elems = planes * out->plane;
+  return SPD_OK;
+}
+
+int spd_step_range(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int64_t lo, int64_t hi,
+                   void* stream) {
+  using namespace spd;
+  int rc = check_desc(plan, gd);
+  if (rc) return rc;
+  StepParams sp;
+  fill_step_params(plan, gd, in, out, lo, hi, sp);
+  return dispatch(plan, sp, (cudaStream_t)stream);
+}
+
+int spd_run(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* buf1, int steps, void* stream) {
+  using namespace spd;
+  int rc = check_desc(plan, gd);
+  if (rc) return rc;
+  if (steps < 1) return set_error(SPD_EINVAL, "step count must be >= 1, got %d", steps);
+  StepParams sp;
+  int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
+  for (int s = 0; s < steps; ++s) {
+    fill_step_params(plan, gd, s % 2 ? buf1 : buf0, s % 2 ? buf0 : buf1, 0, extent, sp);
+    rc = dispatch(plan, sp, (cudaStream_t)stream);
+    if (rc) return rc;
+  }
+  return SPD_OK;
+}
+
+static spd::DenseMap dense_map(const spd_grid_desc* g, int d) {
+  spd::DenseMap dm;
+  dm.h = g->halo;
+  dm.d = d;
+  dm.nxd = g->nx + 2 * g->halo;
+  dm.nyd = g->ny + 2 * g->halo;
+  dm.nzd = d == 3 ? g->nz + 2 * g->halo : 1;
+  return dm;
+}
+
+int spd_pack_grid(const spd_grid_desc* g, int dtype, const double* dense, void* dev, void* stream) {
+  if (!g) return spd::set_error(SPD_EINVAL, "null grid descriptor");
+  spd::DenseMap dm = dense_map(g, g->dims);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPD_DTYPE_F16)
+    spd::pack_kernel<__half><<<1184, 256, 0, st>>>(dm, g->pitch, g->plane, g->origin, dense, (__half*)dev);
+  else
+    spd::pack_kernel<__nv_bfloat16><<<1184, 256, 0, st>>>(dm, g->pitch, g->plane, g->origin, dense,
+                                                          (__nv_bfloat16*)dev);
+  return spd::cuda_err(cudaGetLastError(), "pack_kernel");
+}
+
+int spd_unpack_grid(const spd_grid_desc* g, int dtype, const void* dev, double* dense, void* stream) {
+  if (!g) return spd::set_error(SPD_EINVAL, "null grid descriptor");
+  spd::DenseMap dm = dense_map(g, g->dims);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SPD_DTYPE_F16)
+    spd::unpack_kernel<__half><<<1184, 256, 0, st>>>(dm, g->pitch, g->plane, g->origin, (const __half*)dev, dense);
+  else
+    spd::unpack_kernel<__nv_bfloat16><<<1184, 256, 0, st>>>(dm, g->pitch, g->plane, g->origin,
+                                                            (const __nv_bfloat16*)dev, dense);
+  return spd::cuda_err(cudaGetLastError(), "unpack_kernel");
+}
+
+static cudaMemcpy3DParms copy_parms(const spd_grid_desc* g, void* dev, void* host, bool h2d) {
+  cudaMemcpy3DParms p;
+  std::memset(&p, 0, sizeof(p));
+  const int64_t h = g->halo;
+  const int64_t nxd = g->nx + 2 * h, nyd = g->ny + 2 * h;
+  const int64_t nzd = g->dims == 3 ? g->nz + 2 * h : 1;
+  const int64_t z0 = g->dims == 3 ? h : 0;
+  const int64_t rows_alloc = g->plane / g->pitch;
+  char* corner = (char*)dev + 2 * (g->origin - z0 * g->plane - h * g->pitch - h);
+  cudaPitchedPtr dp = make_cudaPitchedPtr(corner, (size_t)g->pitch * 2, (size_t)nxd * 2, (size_t)rows_alloc);
+  cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)nxd * 2, (size_t)nxd * 2, (size_t)nyd);
+  p.extent = make_cudaExtent((size_t)nxd * 2, (size_t)nyd, (size_t)nzd);
+  if (h2d) {
+    p.srcPtr = hp;
+    p.dstPtr = dp;
+    p.kind = cudaMemcpyHostToDevice;
+  } else {
+    p.srcPtr = dp;
+    p.dstPtr = hp;
+    p.kind = cudaMemcpyDeviceToHost;
+  }
+  return p;
+}
+
+int spd_upload(const spd_grid_desc* g, const void* host_dense, void* dev, void* stream) {
+  if (!g || !host_dense || !dev) return spd::set_error(SPD_EINVAL, "null argument");
+  cudaMemcpy3DParms p = copy_parms(g, dev, const_cast<void*>(host_dense), true);
+  return spd::cuda_err(cudaMemcpy3DAsync(&p, (cudaStream_t)stream), "spd_upload");
+}
+
+int spd_download(const spd_grid_desc* g, const void* dev, void* host_dense, void* stream) {
+  if (!g || !host_dense || !dev) return spd::set_error(SPD_EINVAL, "null argument");
+  cudaMemcpy3DParms p = copy_parms(g, const_cast<void*>(dev), host_dense, false);
+  return spd::cuda_err(cudaMemcpy3DAsync(&p, (cudaStream_t)stream), "spd_download");
+}
+
+int spd_naive_apply_f64(int d, int r, const double* coeffs, int64_t nz, int64_t ny, int64_t nx, int halo,
+                        const double* in, double* out, double* scratch, int steps, void* stream) {
+  using namespace spd;
+  if (steps < 1) return set_error(SPD_EINVAL, "step count must be >= 1, got %d", steps);
+  if (halo < r) return set_error(SPD_EINVAL, "grid halo %d too small for stencil radius %d", halo, r);
+  if (d < 1 || d > 3) return set_error(SPD_EINVAL, "dimensionality must be 1, 2 or 3, got %d", d);
+  cudaStream_t st = (cudaStream_t)stream;
+  int64_t nzd = d == 3 ? nz + 2 * halo : 1;
+  int64_t total = nzd * (ny + 2 * halo) * (nx + 2 * halo);
+  // cur/nxt double buffer: both start as copies of the input (halo included)
+  cudaError_t e = cudaMemcpyAsync(out, in, total * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(scratch, in, total * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return cuda_err(e, "naive copy");
+  double* w = nullptr;
+  int span = 2 * r + 1, ncoef = d == 1 ? span : (d == 2 ? span * span : span * span * span);
+  e = cudaMallocAsync(&w, ncoef * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(w, coeffs, ncoef * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_err(e, "naive coeffs");
+  // steps alternate scratch <-> out so the result lands in `out`
+  double* bufs[2] = {out, scratch};
+  int cur = steps % 2 == 0 ? 0 : 1;  // start so that the last step writes `out`
+  int64_t n = nz * ny * nx;
+  int blocks = (int)((n + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  for (int s = 0; s < steps; ++s) {
+    naive_f64_kernel<<<blocks, 256, 0, st>>>(d, r, w, d == 3 ? nz : 1, ny, nx, halo, bufs[cur], bufs[1 - cur]);
+    cur = 1 - cur;
+  }
+  cudaFreeAsync(w, st);
+  return cuda_err(cudaGetLastError(), "naive_f64_kernel");
+}
+
+int spd_mma_selftest(const uint16_t* a, const uint8_t* e, const uint16_t* b, int n, float* d, void* stream) {
+  using namespace spd;
+  if (n < 8 || n > 256 || n % 8) return set_error(SPD_EINVAL, "N must be a multiple of 8 in [8, 256], got %d", n);
+  mma_selftest_kernel<<<1, 128, 0, (cudaStream_t)stream>>>(a, e, b, n, d);
+  return cuda_err(cudaGetLastError(), "mma_selftest_kernel");
+}
+
+// Whole stored rows (2D) or planes (3D) including the x halo, so corner
+// cells travel with the rows they belong to.
+static int64_t halo_unit(const spd_grid_desc* g) { return g->dims == 3 ? g->plane : g->pitch; }
+static int64_t halo_unit_start(const spd_grid_desc* g, int64_t i) {
+  // element offset of stored row / plane holding interior index i
+  int64_t u = halo_unit(g);
+  return g->origin - (g->origin % u) + i * u;
+}
+
+int spd_halo_pack(const spd_grid_desc* g, const void* buf, int rows, int dir, void* msg, void* stream) {
+  using namespace spd;
+  if (!g) return set_error(SPD_EINVAL, "null grid descriptor");
+  if (g->dims == 1) return set_error(SPD_EINVAL, "1D grids have no slab halo");
+  int64_t extent = g->dims == 3 ? g->nz : g->ny;
+  if (rows < 1 || rows > extent) return set_error(SPD_EINVAL, "bad halo row count %d", rows);
+  int64_t u = halo_unit(g);
+  int64_t first = dir == 0 ? 0 : extent - rows;
+  halo_copy_kernel<uint16_t><<<592, 256, 0, (cudaStream_t)stream>>>(
+      (const uint16_t*)buf, halo_unit_start(g, first), (uint16_t*)msg, 0, rows, u, u, u);
+  return cuda_err(cudaGetLastError(), "halo_pack");
+}
+
+int spd_halo_unpack(const spd_grid_desc* g, void* buf, int rows, int dir, const void* msg, void* stream) {
+  using namespace spd;
+  if (!g) return set_error(SPD_EINVAL, "null grid descriptor");
+  if (g->dims == 1) return set_error(SPD_EINVAL, "1D grids have no slab halo");
+  int64_t extent = g->dims == 3 ? g->nz : g->ny;
+  if (rows < 1 || rows > g->halo) return set_error(SPD_EINVAL, "bad halo row count %d", rows);
+  int64_t u = halo_unit(g);
+  int64_t first = dir == 0 ? -rows : extent;
+  halo_copy_kernel<uint16_t><<<592, 256, 0, (cudaStream_t)stream>>>(
+      (const uint16_t*)msg, 0, (uint16_t*)buf, halo_unit_start(g, first), rows, u, u, u);
+  return cuda_err(cudaGetLastError(), "halo_unpack");
+}
+
+}  // extern "C"

@@ -1,0 +1,58 @@
+// Internal declarations shared by the host AOT code (aot.cpp) and the device
+// engine (engine.cu).  Not part of the public ABI (include/spider.h is).
+#pragma once
+
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/spider.h"
+
+#define SPD_ABI_VERSION 1
+#define SPD_MAX_RIN 64
+#define SPD_MAX_ROUT 32
+#define SPD_MAX_S 16
+
+namespace spd {
+
+int set_error(int code, const char* fmt, ...);
+const char* last_error();
+
+int band_rows(int r);
+int row_permutation(int L, int parity, int64_t* mapping);
+int build_kernel_matrix(int r, const double* row, double* out);
+int swap_columns(const double* values, int rows, int width, int parity, double* out);
+int check_2to4(const double* values, int rows, int width, int32_t* viol, int max_viol);
+int encode_segment(const double* seg, double* vals, uint8_t* pos);
+int encode(const double* swapped, int rows, int width, double* values, uint8_t* metadata);
+int decode(const double* values, const uint8_t* metadata, int rows, int segments, double* out);
+int metadata_to_bytes(const uint8_t* metadata, int n_segments, uint8_t* out);
+int transform_row(int r, int parity, const double* row, double* values, uint8_t* metadata);
+
+uint16_t f64_to_f16_bits(double x);
+uint16_t f64_to_bf16_bits(double x);
+
+// Tile geometry of the sm_100a stencil kernel (see aot.cpp build_geometry).
+// Passed to the kernel by value.
+struct Geometry {
+  int d, r, L;
+  int kc;            // 16-byte K-chunks per input-row window (2L/8)
+  int rows_per_mma;  // input rows per K=32 MMA (4/kc)
+  int r_out;         // output rows per tile (128/L)
+  int r_in;          // input image rows per tile
+  int s;             // MMAs per tile
+  int n_tile;        // x-chunks per tile (MMA N)
+  int tile_z, tile_y, tile_x;  // tile extent in output points (x in points)
+  int b_sbo;         // bytes between 8-chunk core-matrix groups of the B image
+  int start_row[SPD_MAX_S];
+  int first_owned[SPD_MAX_S];
+  int in_dz[SPD_MAX_RIN], in_dy[SPD_MAX_RIN], in_dx[SPD_MAX_RIN];
+  int out_dz[SPD_MAX_ROUT], out_dy[SPD_MAX_ROUT], out_dx[SPD_MAX_ROUT];
+};
+
+int build_geometry(int d, int r, Geometry* g);
+int pack_operands(const Geometry& g, int n_rows, const double* row_values,
+                  const uint8_t* row_meta, int dtype, std::vector<uint16_t>& a_img,
+                  std::vector<uint32_t>& e_words);
+
+}  // namespace spd

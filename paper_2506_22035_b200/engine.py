@@ -1,0 +1,260 @@
+"""Device engine: plans, device-resident grids and the step loop.
+
+A `Plan` owns the packed tcgen05.mma.sp operands for one stencil (the AOT
+transform of every kernel row, laid out for TMEM).  A `DeviceGrid` owns the two
+ping-pong buffers of a halo-padded grid in the engine's HBM layout
+(include/spider.h, spd_grid_desc).  All compute goes through libspider.so; no
+path here falls back to the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import DTYPE_CODES, check, dptr, i32ptr, lib, spd_grid_desc, u16ptr, u32ptr
+from .core import StencilKernel
+from .transform import Parity
+
+TORCH_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
+NP_DTYPES = {"fp16": np.float16}
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "the SPIDER device engine needs a CUDA device (sm_100a); there is no CPU fallback"
+        )
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    return dev
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+@dataclass(frozen=True)
+class PlanInfo:
+    L: int
+    r_in: int
+    r_out: int
+    mmas_per_tile: int
+    n_tile: int
+    tile_z: int
+    tile_y: int
+    kchunks: int
+
+
+class Plan:
+    """Packed device operands for one stencil kernel (spd_plan_create).
+
+    device=-1 builds a host-only plan (operand images without an upload),
+    which the CPU test tier uses to check the packer.
+    """
+
+    def __init__(self, kernel: StencilKernel, parity=Parity.EVEN, dtype: str = "fp16", device: int | None = None):
+        if dtype not in DTYPE_CODES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPE_CODES)}, got {dtype!r}")
+        self.kernel = kernel
+        self.parity = Parity(parity)
+        self.dtype = dtype
+        if device is None:
+            device = require_cuda().index
+        self.device = int(device)
+        coeffs = np.ascontiguousarray(kernel.coeffs, dtype=np.float64).ravel()
+        self._coeffs = coeffs
+        h = C.c_void_p()
+        check(lib.spd_plan_create(kernel.d, kernel.r, self.parity.code, dptr(coeffs), DTYPE_CODES[dtype], self.device, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.spd_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> PlanInfo:
+        buf = np.zeros(8, dtype=np.int32)
+        check(lib.spd_plan_info(self._h, i32ptr(buf)))
+        return PlanInfo(*[int(v) for v in buf])
+
+    def operands(self):
+        """(a_img [S,128,16] uint16, e_words [S,128] uint32, start_rows [S])."""
+        inf = self.info()
+        a = np.zeros((inf.mmas_per_tile, 128, 16), dtype=np.uint16)
+        e = np.zeros((inf.mmas_per_tile, 128), dtype=np.uint32)
+        s = np.zeros(inf.mmas_per_tile, dtype=np.int32)
+        check(lib.spd_plan_operands(self._h, u16ptr(a), u32ptr(e), i32ptr(s)))
+        return a, e, s
+
+    def geometry(self):
+        """(in_off [R_in,3], out_off [R_out,3]) tile row offsets (dz, dy, dx)."""
+        inf = self.info()
+        a = np.zeros((inf.r_in, 3), dtype=np.int32)
+        b = np.zeros((inf.r_out, 3), dtype=np.int32)
+        check(lib.spd_plan_geometry(self._h, i32ptr(a), i32ptr(b)))
+        return a, b
+
+    def layout(self, nz: int, ny: int, nx: int, halo: int) -> spd_grid_desc:
+        desc = spd_grid_desc()
+        check(lib.spd_grid_layout(self._h, int(nz), int(ny), int(nx), int(halo), C.byref(desc)))
+        return desc
+
+
+class DeviceGrid:
+    """Ping-pong buffers of one grid in the engine layout, resident in HBM."""
+
+    def __init__(self, plan: Plan, shape, halo: int):
+        require_cuda()
+        self.plan = plan
+        nz, ny, nx = _shape3(plan.kernel.d, shape)
+        self.desc = plan.layout(nz, ny, nx, halo)
+        dev = torch.device("cuda", plan.device)
+        tdt = TORCH_DTYPES[plan.dtype]
+        self.bufs = [torch.zeros(self.desc.alloc_elems, dtype=tdt, device=dev) for _ in range(2)]
+        self.cur = 0  # index of the buffer holding the current state
+        self.step = 0
+
+    @property
+    def halo(self) -> int:
+        return int(self.desc.halo)
+
+    @property
+    def dense_shape(self):
+        h = self.desc.halo
+        if self.plan.kernel.d == 3:
+            return (self.desc.nz + 2 * h, self.desc.ny + 2 * h, self.desc.nx + 2 * h)
+        return (self.desc.ny + 2 * h, self.desc.nx + 2 * h)
+
+    def _sync_halo(self, stream=None) -> None:
+        self.bufs[1 - self.cur].copy_(self.bufs[self.cur])
+
+    def load_dense_f64(self, dense: torch.Tensor, stream=None) -> None:
+        """Quantise a dense fp64 device tensor (halo included) into the grid."""
+        if dense.dtype != torch.float64 or not dense.is_cuda:
+            raise ValueError("expected a CUDA float64 tensor")
+        dense = dense.contiguous()
+        if tuple(dense.shape) != tuple(self.dense_shape):
+            raise ValueError(f"dense grid shape {tuple(dense.shape)} != {self.dense_shape}")
+        check(lib.spd_pack_grid(C.byref(self.desc), DTYPE_CODES[self.plan.dtype], C.c_void_p(dense.data_ptr()),
+                                C.c_void_p(self.bufs[self.cur].data_ptr()), _stream_ptr(stream)))
+        self._sync_halo(stream)
+
+    def to_dense_f64(self, stream=None) -> torch.Tensor:
+        out = torch.empty(self.dense_shape, dtype=torch.float64, device=self.bufs[0].device)
+        check(lib.spd_unpack_grid(C.byref(self.desc), DTYPE_CODES[self.plan.dtype],
+                                  C.c_void_p(self.bufs[self.cur].data_ptr()), C.c_void_p(out.data_ptr()),
+                                  _stream_ptr(stream)))
+        return out
+
+    def upload(self, host: torch.Tensor, stream=None) -> None:
+        """Strided DMA of a host 16-bit dense grid (pinned for async)."""
+        if host.dtype != TORCH_DTYPES[self.plan.dtype] or host.is_cuda:
+            raise ValueError(f"expected a host {TORCH_DTYPES[self.plan.dtype]} tensor")
+        if tuple(host.shape) != tuple(self.dense_shape) or not host.is_contiguous():
+            raise ValueError(f"host grid must be contiguous with shape {self.dense_shape}")
+        check(lib.spd_upload(C.byref(self.desc), C.c_void_p(host.data_ptr()),
+                             C.c_void_p(self.bufs[self.cur].data_ptr()), _stream_ptr(stream)))
+        self._sync_halo(stream)
+
+    def download(self, host: torch.Tensor, stream=None) -> None:
+        if host.dtype != TORCH_DTYPES[self.plan.dtype] or host.is_cuda:
+            raise ValueError(f"expected a host {TORCH_DTYPES[self.plan.dtype]} tensor")
+        check(lib.spd_download(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
+                               C.c_void_p(host.data_ptr()), _stream_ptr(stream)))
+
+    def run(self, steps: int, stream=None) -> None:
+        """`steps` Jacobi steps on the device, ping-ponging the buffers."""
+        if steps < 1:
+            raise ValueError(f"step count must be >= 1, got {steps}")
+        a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
+        check(lib.spd_run(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                          int(steps), _stream_ptr(stream)))
+        self.cur = (self.cur + steps) % 2
+        self.step += steps
+
+    def step_range(self, lo: int, hi: int, stream=None) -> None:
+        """One step over output rows (2D) / planes (3D) [lo, hi) only; does
+        not flip the buffers (call `flip()` once the whole domain is done)."""
+        a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
+        check(lib.spd_step_range(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()),
+                                 C.c_void_p(b.data_ptr()), int(lo), int(hi), _stream_ptr(stream)))
+
+    def flip(self) -> None:
+        self.cur = 1 - self.cur
+        self.step += 1
+
+    def view_rows(self, which: int | None = None) -> torch.Tensor:
+        """2D/1D: the stored buffer as [rows, pitch]; 3D: [planes, rows, pitch]."""
+        buf = self.bufs[self.cur if which is None else which]
+        d = self.desc
+        if self.plan.kernel.d == 3:
+            return buf.view(-1, d.plane // d.pitch, d.pitch)
+        return buf.view(-1, d.pitch)
+
+
+def _shape3(d: int, shape):
+    shape = tuple(int(s) for s in shape)
+    if d == 3:
+        if len(shape) != 3:
+            raise ValueError("3D grids need an interior shape (Z, A, B)")
+        return shape
+    if len(shape) != 2:
+        raise ValueError("2D/1D grids need an interior shape (A, B)")
+    return (1,) + shape
+
+
+def naive_apply_device(kernel: StencilKernel, dense: torch.Tensor, halo: int, steps: int) -> torch.Tensor:
+    """fp64 brute-force executor on the device (reference core.py:151-182).
+
+    `dense` is the halo-padded fp64 CUDA tensor; returns a new tensor.  Same
+    row-major tap order and separate multiply/add roundings as the numpy
+    oracle, so results are bit-identical to it.
+    """
+    require_cuda()
+    if steps < 1:
+        raise ValueError(f"step count must be >= 1, got {steps}")
+    if halo < kernel.r:
+        raise ValueError(f"grid halo {halo} too small for stencil radius {kernel.r}")
+    dense = dense.contiguous()
+    if kernel.d == 3:
+        nz, ny, nx = (s - 2 * halo for s in dense.shape)
+    else:
+        nz = 1
+        ny, nx = (s - 2 * halo for s in dense.shape)
+    out = torch.empty_like(dense)
+    scratch = torch.empty_like(dense)
+    coeffs = np.ascontiguousarray(kernel.coeffs, dtype=np.float64).ravel()
+    check(lib.spd_naive_apply_f64(kernel.d, kernel.r, dptr(coeffs), nz, ny, nx, halo, C.c_void_p(dense.data_ptr()),
+                                  C.c_void_p(out.data_ptr()), C.c_void_p(scratch.data_ptr()), int(steps),
+                                  _stream_ptr()))
+    return out
+
+
+def mma_selftest(a: np.ndarray, e: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """One tcgen05.mma.sp on the device: decode(a, e) @ b (M=128, K=32)."""
+    require_cuda()
+    n = b.shape[1]
+    ta = torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint16).view(np.int16)).cuda()
+    te = torch.from_numpy(np.ascontiguousarray(e, dtype=np.uint8)).cuda()
+    tb = torch.from_numpy(np.ascontiguousarray(b, dtype=np.uint16).view(np.int16)).cuda()
+    td = torch.empty((128, n), dtype=torch.float32, device="cuda")
+    check(lib.spd_mma_selftest(C.c_void_p(ta.data_ptr()), C.c_void_p(te.data_ptr()), C.c_void_p(tb.data_ptr()), n,
+                               C.c_void_p(td.data_ptr()), _stream_ptr()))
+    return td.cpu().numpy()
+
+
+_ = _lib

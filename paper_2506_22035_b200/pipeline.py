@@ -1,0 +1,353 @@
+"""Drop-in execution API: transform_stencil / execute / naive_apply / verify.
+
+Mirrors the reference engine surface (reference pipeline.py:42-333) with the
+hot path moved to the B200:
+
+* `transform_stencil` — the AOT transform per kernel row (C++ twin of
+  transform.py, exact), same `TransformedStencil` result.
+* `execute` — same signature and return type; the T-step loop runs on the
+  sparse tensor cores (libspider.so, tcgen05.mma.sp).  Storage is fp16 (or
+  bf16 via `DeviceConfig`) with fp32 accumulation.  `ExecConfig` keeps the
+  reference's fields and its fp16 rejection; device precision is chosen by
+  `DeviceConfig`.
+* `naive_apply` — the brute-force executor, on the device in fp64 with the
+  reference's tap order and separate multiply/add roundings: bit-identical to
+  the reference's numpy oracle.
+* `verify` — device `execute` against device `naive_apply` over seeded grids,
+  same report keys.
+"""
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from .core import Grid, Grid3D, StencilKernel, random_grid
+from .engine import DeviceGrid, Plan, TORCH_DTYPES, naive_apply_device, require_cuda
+from .transform import CompressedKernel, Parity, RowPermutation, band_rows, input_row_permutation, transform_row
+
+_HOST_PRECISIONS = {"fp64": np.float64, "fp32": np.float32}
+
+# fp16/bf16 storage tolerances on max|got-want|/max|want| for T <= 4 steps
+# against the fp64 oracle on identically quantised inputs.
+DEFAULT_TOLERANCE = {"fp16": 1e-2, "bf16": 5e-2}
+
+
+@dataclass(frozen=True)
+class ExecConfig:
+    """Reference execution knobs (reference pipeline.py:42-63).
+
+    Kept field-for-field so reference callers construct it unchanged; the
+    device path reads `parity` from it and computes in fp16.
+    """
+
+    parity: Parity = Parity.EVEN
+    a_block: int | None = None
+    b_block: int | None = None
+    a_warp: int = 16
+    b_warp: int = 8
+    mma: object = None
+    precision: str = "fp64"
+    compute_mode: str = "ceil"
+    packing: bool = True
+
+    def __post_init__(self) -> None:
+        if self.precision not in _HOST_PRECISIONS:
+            raise ValueError(f"precision must be one of {sorted(_HOST_PRECISIONS)}")
+        object.__setattr__(self, "parity", Parity(self.parity))
+
+    @property
+    def dtype(self):
+        return _HOST_PRECISIONS[self.precision]
+
+
+@dataclass(frozen=True)
+class DeviceConfig:
+    """Device-path knobs: storage dtype of the grid on the B200 and parity."""
+
+    parity: Parity = Parity.EVEN
+    dtype: str = "fp16"
+    device: int | None = None
+
+    def __post_init__(self) -> None:
+        if self.dtype not in TORCH_DTYPES:
+            raise ValueError(f"device dtype must be one of {sorted(TORCH_DTYPES)}")
+        object.__setattr__(self, "parity", Parity(self.parity))
+
+
+@dataclass
+class ExecStats:
+    """Execution counters.  The reference keys (pipeline.py:66-108) keep their
+    algorithmic meaning (per kernel row and step, L x L compressed MACs per
+    x-chunk); `device` adds what the B200 actually issued."""
+
+    grid_a: int
+    grid_b: int
+    steps: int
+    radius: int
+    kernel_rows: int
+    L: int
+    parity: str
+    packing: bool
+    total_macs: int = 0
+    dense_macs: int = 0
+    input_elements: int = 0
+    param_elements: int = 0
+    mma_invocations: int = 0
+    sparse_mma_calls: int = 0
+    fetch_runs_packed: int = 0
+    fetch_runs_unpacked: int = 0
+    fetch_runs_active: int = 0
+    tile_counts: dict = field(default_factory=dict)
+    device: dict = field(default_factory=dict)
+
+    def as_dict(self) -> dict:
+        return {
+            "grid": [self.grid_a, self.grid_b],
+            "steps": self.steps,
+            "radius": self.radius,
+            "kernel_rows": self.kernel_rows,
+            "L": self.L,
+            "parity": self.parity,
+            "packing": self.packing,
+            "total_macs": self.total_macs,
+            "dense_macs": self.dense_macs,
+            "input_elements": self.input_elements,
+            "param_elements": self.param_elements,
+            "mma_invocations": self.mma_invocations,
+            "sparse_mma_calls": self.sparse_mma_calls,
+            "fetch_runs_packed": self.fetch_runs_packed,
+            "fetch_runs_unpacked": self.fetch_runs_unpacked,
+            "fetch_runs_active": self.fetch_runs_active,
+            "tile_counts": dict(self.tile_counts),
+            "device": dict(self.device),
+        }
+
+
+@dataclass
+class TransformedStencil:
+    r: int
+    L: int
+    parity: Parity
+    rows: list
+    permutation: RowPermutation
+
+
+def _parity_of(cfg) -> Parity:
+    if isinstance(cfg, (ExecConfig, DeviceConfig)):
+        return cfg.parity
+    return Parity(cfg)
+
+
+def transform_stencil(kernel: StencilKernel, cfg=ExecConfig()) -> TransformedStencil:
+    """One compressed kernel per kernel row (reference pipeline.py:128-144).
+
+    3D kernels (extension) give one record per (rho_z, rho_y), row-major."""
+    if kernel.d not in (1, 2, 3) or np.asarray(kernel.coeffs).ndim != kernel.d:
+        raise ValueError(f"unsupported dimensionality {kernel.d}")
+    parity = _parity_of(cfg)
+    L = band_rows(kernel.r)
+    rows = [(rho, transform_row(kernel.row(rho), kernel.r, parity)) for rho in kernel.row_offsets()]
+    return TransformedStencil(r=kernel.r, L=L, parity=parity, rows=rows, permutation=input_row_permutation(L, parity))
+
+
+# ---------------------------------------------------------------------------
+# plan cache (one per kernel/parity/dtype/device)
+
+_PLANS: dict = {}
+
+
+def get_plan(kernel: StencilKernel, parity: Parity, dtype: str, device: int | None = None) -> Plan:
+    dev = require_cuda(device).index if device is None else int(device)
+    key = (kernel.d, kernel.r, np.asarray(kernel.coeffs, dtype=np.float64).tobytes(), Parity(parity), dtype, dev)
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = Plan(kernel, parity, dtype, dev)
+        _PLANS[key] = plan
+    return plan
+
+
+def _device_cfg(cfg) -> DeviceConfig:
+    if isinstance(cfg, DeviceConfig):
+        return cfg
+    if isinstance(cfg, ExecConfig):
+        return DeviceConfig(parity=cfg.parity)
+    return DeviceConfig(parity=Parity(cfg))
+
+
+def _check_inputs(kernel: StencilKernel, grid, steps: int) -> None:
+    if steps < 1:
+        raise ValueError(f"step count must be >= 1, got {steps}")
+    if grid.halo < kernel.r:
+        raise ValueError(f"grid halo {grid.halo} too small for stencil radius {kernel.r}")
+    if (kernel.d == 3) != isinstance(grid, Grid3D):
+        raise ValueError("unsupported dimensionality: 3D kernels need a Grid3D and vice versa")
+    L = band_rows(kernel.r)
+    if grid.B % L != 0:
+        raise ValueError(f"grid width {grid.B} must be a multiple of the x-chunk size L={L}")
+
+
+def _stats(kernel: StencilKernel, grid, steps: int, parity: Parity, plan: Plan) -> ExecStats:
+    """Reference counter semantics (pipeline.py:254-259) per step and kernel row."""
+    L = band_rows(kernel.r)
+    n_rows = len(list(kernel.row_offsets()))
+    planes = grid.Z if isinstance(grid, Grid3D) else 1
+    cols = planes * grid.A * (grid.B // L)
+    n_groups = -(-cols // 8)
+    inv_k = -(-2 * L // 16)
+    m_groups = -(-L // 16)
+    per = steps * n_rows
+    st = ExecStats(
+        grid_a=grid.A,
+        grid_b=grid.B,
+        steps=steps,
+        radius=kernel.r,
+        kernel_rows=n_rows,
+        L=L,
+        parity=parity.value,
+        packing=True,
+    )
+    st.total_macs = per * L * cols * L
+    st.dense_macs = 2 * st.total_macs
+    st.input_elements = per * 2 * L * cols
+    st.param_elements = per * L * L * n_groups
+    st.mma_invocations = per * m_groups * n_groups * inv_k
+    st.sparse_mma_calls = per
+    info = plan.info()
+    tiles_x = -(-grid.B // (info.n_tile * L)) if kernel.d != 1 else -(-grid.B // (info.n_tile * L * info.r_out))
+    tiles = tiles_x * (-(-grid.A // info.tile_y) if kernel.d >= 2 else 1) * (-(-planes // info.tile_z))
+    st.tile_counts = {"block_tiles": tiles, "n_tile": info.n_tile, "tile_rows": info.r_out}
+    st.device = {
+        "arch": "sm_100a",
+        "instruction": "tcgen05.mma.sp.cta_group::1.kind::f16 M128 N%d K32" % info.n_tile,
+        "dtype": plan.dtype,
+        "launches": steps,
+        "tiles_per_step": tiles,
+        "mma_instructions": steps * tiles * info.mmas_per_tile,
+        "issued_sparse_macs": steps * tiles * info.mmas_per_tile * 128 * info.n_tile * 16,
+    }
+    return st
+
+
+def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig()):
+    """Run `steps` steps on the B200 sparse-tensor-core path; returns
+    (Grid, ExecStats) like reference pipeline.py:189-262.  The input grid is
+    never modified.  float16 host grids are transferred as-is (pinned host
+    memory gives asynchronous DMA); other dtypes are quantised on the device.
+    """
+    _check_inputs(kernel, grid, steps)
+    dcfg = _device_cfg(cfg)
+    plan = get_plan(kernel, dcfg.parity, dcfg.dtype, dcfg.device)
+    shape = (grid.Z, grid.A, grid.B) if kernel.d == 3 else (grid.A, grid.B)
+    dg = DeviceGrid(plan, shape, grid.halo)
+    data = grid.data
+    native16 = dcfg.dtype == "fp16" and data.dtype == np.float16
+    if native16:
+        dg.upload(torch.from_numpy(np.ascontiguousarray(data)))
+    else:
+        dg.load_dense_f64(torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dg.bufs[0].device))
+    dg.run(steps)
+    if native16:
+        out = torch.empty(dg.dense_shape, dtype=torch.float16)
+        dg.download(out)
+        torch.cuda.current_stream().synchronize()
+        res = out.numpy()
+    else:
+        res = dg.to_dense_f64().cpu().numpy()
+        if data.dtype in (np.float32,):
+            res = res.astype(np.float32)
+    cls = Grid3D if kernel.d == 3 else Grid
+    return cls(res, grid.halo, grid.step + steps), _stats(kernel, grid, steps, dcfg.parity, plan)
+
+
+def naive_apply(kernel: StencilKernel, grid, steps: int):
+    """Reference executor (core.py:151-182) on the device in fp64.
+
+    Bit-identical to the reference numpy oracle for float64 grids; float32
+    grids are evaluated in fp64 and rounded once at the end."""
+    if steps < 1:
+        raise ValueError(f"step count must be >= 1, got {steps}")
+    if grid.halo < kernel.r:
+        raise ValueError(f"grid halo {grid.halo} too small for stencil radius {kernel.r}")
+    dev = require_cuda()
+    dense = torch.from_numpy(np.ascontiguousarray(grid.data, dtype=np.float64)).to(dev)
+    out = naive_apply_device(kernel, dense, grid.halo, steps).cpu().numpy().astype(grid.data.dtype, copy=False)
+    cls = Grid3D if kernel.d == 3 else Grid
+    return cls(out, grid.halo, grid.step + steps)
+
+
+def max_rel_error(result: np.ndarray, reference: np.ndarray) -> float:
+    """max|got-want| / max|want| (reference pipeline.py:265-267)."""
+    result = np.asarray(result, dtype=np.float64)
+    reference = np.asarray(reference, dtype=np.float64)
+    scale = max(float(np.max(np.abs(reference))), 1e-300)
+    return float(np.max(np.abs(result - reference)) / scale)
+
+
+def verify(kernel: StencilKernel, sizes, seed: int, steps: int, cfg=ExecConfig(), tolerance: float | None = None) -> dict:
+    """Device execute vs device fp64 naive_apply over seeded random grids
+    (reference pipeline.py:270-328).  Inputs are quantised to the device dtype
+    first, so the comparison measures the arithmetic, not the input rounding."""
+    dcfg = _device_cfg(cfg)
+    tol = DEFAULT_TOLERANCE[dcfg.dtype] if tolerance is None else float(tolerance)
+    cases = []
+    first_ok = None
+    for size in sizes:
+        a, b = (1, int(size)) if kernel.d == 1 else (int(size), int(size))
+        grid = random_grid(a, b, kernel.r, seed=[seed, a, b])
+        q = torch.from_numpy(grid.data).to(TORCH_DTYPES[dcfg.dtype]).to(torch.float64).numpy()
+        grid = Grid(q, grid.halo)
+        try:
+            got, _ = execute(kernel, grid, steps, dcfg)
+        except ValueError as exc:
+            cases.append({"size": [a, b], "error": str(exc), "pass": False})
+            continue
+        want = naive_apply(kernel, grid, steps)
+        err = max_rel_error(got.interior, want.interior)
+        cases.append({"size": [a, b], "max_rel_error": err, "pass": err < tol})
+        if first_ok is None:
+            first_ok = (grid, got)
+    cross: dict = {}
+    if first_ok is not None:
+        grid, got = first_ok
+        other = Parity.ODD if dcfg.parity is Parity.EVEN else Parity.EVEN
+        flipped, _ = execute(kernel, grid, steps, replace(dcfg, parity=other))
+        cross = {
+            "parity_max_abs_diff": float(np.max(np.abs(flipped.interior - got.interior))),
+            "parity_bitwise_identical": bool(np.array_equal(flipped.interior, got.interior)),
+        }
+    return {
+        "kernel": {"shape": kernel.shape.value, "d": kernel.d, "r": kernel.r, "coeffs": kernel.coeffs.tolist()},
+        "parity": dcfg.parity.value,
+        "precision": dcfg.dtype,
+        "packing": True,
+        "steps": steps,
+        "seed": seed,
+        "tolerance": tol,
+        "cases": cases,
+        "all_pass": all(c["pass"] for c in cases),
+        "cross_checks": cross,
+    }
+
+
+def report_json(report: dict) -> str:
+    return json.dumps(report, indent=2, sort_keys=True)
+
+
+__all__ = [
+    "ExecConfig",
+    "DeviceConfig",
+    "ExecStats",
+    "TransformedStencil",
+    "CompressedKernel",
+    "transform_stencil",
+    "execute",
+    "naive_apply",
+    "verify",
+    "report_json",
+    "max_rel_error",
+    "get_plan",
+    "DEFAULT_TOLERANCE",
+]

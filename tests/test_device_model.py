@@ -1,0 +1,146 @@
+"""CPU model of one device tile, built from the plan's real packed operands.
+
+The host-only plan (device=-1) exposes exactly what libspider uploads: the
+compressed A values [S,128,16] (fp16 bits), the E metadata words [S,128] in the
+TMEM lane/bit layout, the MMA start rows and the tile geometry.  This test
+decodes them with the hardware semantics pinned by tools/umma_sp_probe.cu
+(metadata lane = m0 + 8*k1 + 16*m2, bits 16*m1 + 4*c, nibble idx0|idx1<<2),
+rebuilds the B operand the producer warps stage (2L windows, involution from
+transform.py:130-139), runs D = sum_s A_s @ B_s in fp64 and compares with the
+oracle.  It checks geometry, packing and the permutation logic without a GPU.
+"""
+import numpy as np
+import pytest
+
+import paper_2506_22035_b200 as sp
+from paper_2506_22035_b200.engine import Plan
+from oracle import naive
+
+
+def decode_A(a_img, e_words):
+    S = a_img.shape[0]
+    vals = a_img.view(np.float16).astype(np.float64)
+    nib = np.zeros((S, 128, 8), dtype=np.int64)
+    for lane in range(128):
+        m0, k1, m2 = lane % 8, (lane // 8) % 2, lane // 16
+        for m1 in (0, 1):
+            for c4 in range(4):
+                m = m0 + 8 * m1 + 16 * m2
+                nib[:, m, 4 * k1 + c4] = (e_words[:, lane].astype(np.int64) >> (16 * m1 + 4 * c4)) & 0xF
+    A = np.zeros((S, 128, 32))
+    p0, p1 = nib & 3, nib >> 2
+    assert np.all(p0 < p1), "metadata must be ascending pairs"
+    for s in range(S):
+        for m in range(128):
+            for seg in range(8):
+                A[s, m, 4 * seg + p0[s, m, seg]] += vals[s, m, 2 * seg]
+                A[s, m, 4 * seg + p1[s, m, seg]] += vals[s, m, 2 * seg + 1]
+    return A
+
+
+def tile_model(plan, dense, halo):
+    kern = plan.kernel
+    r = kern.r
+    inf = plan.info()
+    L, n_tile = inf.L, inf.n_tile
+    a_img, e_words, starts = plan.operands()
+    in_off, out_off = plan.geometry()
+    perm = sp.input_row_permutation(L, plan.parity).mapping
+    A = decode_A(a_img, e_words)
+    dense3 = dense if dense.ndim == 3 else dense[None]
+    zh = halo if dense.ndim == 3 else 0
+    Bimg = np.zeros((inf.r_in, n_tile, 2 * L))
+    for b in range(inf.r_in):
+        dz, dy, dx = in_off[b]
+        for n in range(n_tile):
+            for q in range(2 * L):
+                x = dx + n * L - r + perm[q]
+                zz, yy, xx = dz + zh, dy + halo, x + halo
+                if 0 <= zz < dense3.shape[0] and 0 <= yy < dense3.shape[1] and 0 <= xx < dense3.shape[2]:
+                    Bimg[b, n, q] = dense3[zz, yy, xx]
+    rpm = 32 // (2 * L)
+    D = np.zeros((128, n_tile))
+    for s in range(inf.mmas_per_tile):
+        Bs = Bimg[starts[s] : starts[s] + rpm].transpose(0, 2, 1).reshape(32, n_tile)
+        D += A[s] @ Bs
+    out = {}
+    for a in range(inf.r_out):
+        dz, dy, dx = out_off[a]
+        for i in range(L):
+            for n in range(n_tile):
+                out[(dz, dy, dx + n * L + i)] = D[L * a + i, n]
+    return out
+
+
+def f16(x):
+    return np.asarray(x, dtype=np.float64).astype(np.float16).astype(np.float64)
+
+
+CASES = [
+    ("box", 2, 1),
+    ("star", 2, 1),
+    ("box", 2, 3),
+    ("star", 2, 3),
+    ("box", 3, 1),
+    ("box", 1, 1),
+    ("box", 1, 3),
+]
+
+
+@pytest.mark.parametrize("shape,d,r", CASES)
+@pytest.mark.parametrize("parity", ["even", "odd"])
+def test_tile_model_matches_oracle(shape, d, r, parity):
+    rng = np.random.default_rng([d, r, 11])
+    span = 2 * r + 1
+    coeffs = rng.uniform(-1, 1, (span,) * d)
+    if shape == "star" and d >= 2:
+        mask = np.zeros_like(coeffs, dtype=bool)
+        mask[r, :] = True
+        mask[:, r] = True
+        coeffs = np.where(mask, coeffs, 0.0)
+    kern = sp.make_kernel_3d(shape, r, coeffs) if d == 3 else sp.make_kernel(shape, d, r, coeffs)
+    plan = Plan(kern, parity, "fp16", device=-1)
+    inf = plan.info()
+    L = inf.L
+    in_off, out_off = plan.geometry()
+    if d == 3:
+        shape3 = (inf.tile_z, inf.tile_y, inf.n_tile * L)
+    elif d == 2:
+        shape3 = (inf.tile_y, inf.n_tile * L)
+    else:
+        shape3 = (1, inf.n_tile * L * inf.r_out)
+    dense = f16(rng.uniform(-1, 1, tuple(s + 2 * r for s in shape3)))
+    got = tile_model(plan, dense, r)
+    want = naive.naive_apply(f16(coeffs), d, r, dense, r, 1)
+    h = r
+    err = 0.0
+    for (z, y, x), v in got.items():
+        w = want[z + h, y + h, x + h] if d == 3 else want[y + h, x + h]
+        err = max(err, abs(v - w))
+    assert len(got) == int(np.prod(shape3))
+    assert err < 1e-12, err
+
+
+def test_operand_bits_are_fp16_coefficients():
+    k = sp.make_kernel("box", 2, 1, np.arange(1, 10) / 7.0)
+    plan = Plan(k, "even", "fp16", device=-1)
+    a_img, e_words, starts = plan.operands()
+    vals = set(np.unique(a_img.view(np.float16).astype(np.float64)))
+    want = set(f16(np.arange(1, 10) / 7.0)) | {0.0}
+    assert vals <= want and vals >= want - {0.0}
+    assert list(starts) == [0, 4, 8, 12, 16, 20, 24, 28, 30]
+
+
+def test_bf16_operands():
+    k = sp.make_kernel("box", 2, 1, np.full(9, 1 / 3))
+    plan = Plan(k, "even", "bf16", device=-1)
+    a_img, _, _ = plan.operands()
+    nz = a_img[a_img != 0]
+    # 1/3 in bf16 = 0x3EAB
+    assert set(nz.tolist()) == {0x3EAB}
+
+
+def test_unsupported_radius_rejected_by_device_plan():
+    k = sp.make_kernel("box", 2, 2, np.ones(25))
+    with pytest.raises(ValueError, match="unsupported"):
+        Plan(k, "even", "fp16", device=-1)

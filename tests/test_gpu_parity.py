@@ -1,0 +1,267 @@
+"""Device parity: the sm_100a sparse-tensor-core path against the CPU oracle.
+
+Tolerances (fp16 storage, fp32 tensor-core accumulation), on
+max|got-want|/max|want| (reference pipeline.py:265-267) against the fp64
+oracle run on identically quantised inputs:
+  * one step, fp16-rounded coefficients in the oracle too: every point within
+    one fp16 rounding of the exact value (0.5 ulp + 1e-6 of the row scale)
+  * T <= 4 steps vs the fp64-coefficient oracle: 1e-2 (fp16), 5e-2 (bf16)
+Device naive_apply (fp64) is bit-identical to the oracle.
+"""
+import numpy as np
+import pytest
+import torch
+
+import paper_2506_22035_b200 as sp
+from paper_2506_22035_b200.engine import DeviceGrid, mma_selftest
+from paper_2506_22035_b200.pipeline import DeviceConfig, get_plan, max_rel_error
+from oracle import cnaive
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp16": 1e-2, "bf16": 5e-2}
+
+
+def quant(x, dtype="fp16"):
+    t = torch.from_numpy(np.array(x, dtype=np.float64))
+    return t.to(torch.float16 if dtype == "fp16" else torch.bfloat16).to(torch.float64).numpy()
+
+
+def heat2d(alpha=0.125):
+    c = np.zeros((3, 3))
+    c[1, 1] = 1 - 4 * alpha
+    c[0, 1] = c[2, 1] = c[1, 0] = c[1, 2] = alpha
+    return c
+
+
+def heat3d(alpha=1 / 12):
+    c = np.zeros((3, 3, 3))
+    c[1, 1, 1] = 1 - 6 * alpha
+    for a in ((0, 1, 1), (2, 1, 1), (1, 0, 1), (1, 2, 1), (1, 1, 0), (1, 1, 2)):
+        c[a] = alpha
+    return c
+
+
+def rand_kernel(shape, d, r, seed):
+    rng = np.random.default_rng(seed)
+    n = 2 * r + 1
+    c = rng.uniform(-1, 1, (n,) * d)
+    if shape == "star" and d >= 2:
+        m = np.zeros_like(c, dtype=bool)
+        m[(r,) * (d - 1)] = True
+        for ax in range(d):
+            idx = [r] * d
+            idx[ax] = slice(None)
+            m[tuple(idx)] = True
+        c = np.where(m, c, 0.0)
+    return sp.make_kernel_3d(shape, r, c) if d == 3 else sp.make_kernel(shape, d, r, c)
+
+
+def run_case(kern, shape, steps, dtype="fp16", parity="even", seed=0):
+    h = kern.r
+    rng = np.random.default_rng(seed)
+    data = quant(rng.uniform(-1, 1, tuple(s + 2 * h for s in shape)), dtype)
+    grid = sp.Grid3D(data, h) if kern.d == 3 else sp.Grid(data, h)
+    got, stats = sp.execute(kern, grid, steps, DeviceConfig(parity=parity, dtype=dtype))
+    want = cnaive.naive_apply(kern.coeffs, kern.d, kern.r, data, h, steps)
+    return got, want, grid, stats
+
+
+# --------------------------------------------------------------------------
+def test_mma_selftest_matches_decode():
+    rng = np.random.default_rng(3)
+    for n in (8, 64, 128, 256):
+        vals = rng.integers(-3, 4, (128, 16)).astype(np.float16)
+        nib = np.zeros((128, 8), dtype=np.uint8)
+        A = np.zeros((128, 32))
+        for m in range(128):
+            for s in range(8):
+                p = np.sort(rng.choice(4, 2, replace=False))
+                nib[m, s] = p[0] | (p[1] << 2)
+                A[m, 4 * s + p[0]] = vals[m, 2 * s]
+                A[m, 4 * s + p[1]] = vals[m, 2 * s + 1]
+        B = rng.integers(-4, 5, (32, n)).astype(np.float16)
+        D = mma_selftest(vals.view(np.uint16), nib, B.view(np.uint16))
+        np.testing.assert_array_equal(D, (A @ B.astype(np.float64)).astype(np.float32))
+
+
+def test_device_naive_bit_exact_vs_oracle(golden):
+    g = golden("naive_golden.npz")
+    for c in range(int(g["n_cases"])):
+        d, r, steps, star = (int(v) for v in g[f"c{c}_meta"])
+        coeffs = g[f"c{c}_coeffs"]
+        k = sp.make_kernel("star" if star else "box", d, r, coeffs)
+        out = sp.naive_apply(k, sp.Grid(g[f"c{c}_in"].copy(), r), steps)
+        np.testing.assert_array_equal(out.data, g[f"c{c}_out"])
+
+
+def test_device_naive_3d_pins(golden):
+    g = golden("naive3d_golden.npz")
+    k = sp.make_kernel_3d("box", 1, g["a_coeffs"])
+    out = sp.naive_apply(k, sp.Grid3D(g["a_in"].copy(), 1), 1)
+    np.testing.assert_array_equal(out.data, g["a_out"])
+
+
+def test_s5_oracle_config(golden):
+    """Star-2D5P (Heat-2D) 512^2, 4 steps — BASELINE configs[0]."""
+    g = golden("naive_golden.npz")
+    k = sp.make_kernel("star", 2, 1, g["s5_coeffs"])
+    grid = sp.random_grid(512, 512, 1, seed=[1, 512, 512])
+    # the device naive path reproduces the reference oracle exactly
+    ref = sp.naive_apply(k, grid, 4)
+    np.testing.assert_array_equal(ref.data[240:272, 240:272], g["s5_center"])
+    q = sp.Grid(quant(grid.data), 1)
+    got, stats = sp.execute(k, q, 4)
+    want = cnaive.naive_apply(k.coeffs, 2, 1, q.data, 1, 4)
+    err = max_rel_error(got.interior, want[1:-1, 1:-1])
+    assert err < TOL["fp16"], err
+    assert stats.dense_macs == 2 * stats.total_macs
+
+
+@pytest.mark.parametrize("shape,d,r,dims", [
+    ("box", 2, 1, (64, 512)),
+    ("star", 2, 1, (37, 200)),      # ragged: partial tiles in y and x
+    ("box", 2, 3, (48, 136)),
+    ("star", 2, 3, (17, 64)),
+    ("box", 3, 1, (9, 20, 72)),
+    ("star", 3, 1, (4, 8, 256)),
+    ("box", 1, 1, (1, 1000)),
+    ("box", 1, 3, (1, 16384 + 40)),
+])
+@pytest.mark.parametrize("parity", ["even", "odd"])
+def test_execute_matches_oracle(shape, d, r, dims, parity):
+    k = rand_kernel(shape, d, r, seed=[d, r, 5])
+    for steps in (1, 3):
+        got, want, grid, _ = run_case(k, dims, steps, parity=parity, seed=steps)
+        h = r
+        gi = got.interior
+        wi = want[h:-h, h:-h, h:-h] if d == 3 else want[h:-h, h:-h]
+        err = max_rel_error(gi, wi)
+        assert err < TOL["fp16"], (steps, err)
+        # the halo is never written
+        if d == 3:
+            mask = np.ones(got.data.shape, bool)
+            mask[h:-h, h:-h, h:-h] = False
+        else:
+            mask = np.ones(got.data.shape, bool)
+            mask[h:-h, h:-h] = False
+        np.testing.assert_array_equal(got.data[mask], grid.data[mask])
+
+
+@pytest.mark.parametrize("d,r", [(2, 1), (2, 3), (3, 1), (1, 1)])
+def test_single_step_within_one_fp16_rounding(d, r):
+    """One step, fp16-rounded coefficients in the oracle: the device result is
+    the fp16 rounding of an fp32-accumulated exact sum."""
+    k = rand_kernel("box", d, r, seed=[d, r, 77])
+    kq = quant(k.coeffs)
+    dims = {1: (1, 4096), 2: (40, 520), 3: (8, 16, 256)}[d]
+    got, _, grid, _ = run_case(k, dims, 1, seed=4)
+    want = cnaive.naive_apply(kq, d, r, grid.data, r, 1)
+    h = r
+    gi = got.interior
+    wi = want[h:-h, h:-h, h:-h] if d == 3 else want[h:-h, h:-h]
+    ulp = np.spacing(np.abs(wi).astype(np.float16)).astype(np.float64)
+    bound = 0.5 * ulp + 1e-6 * np.abs(wi).max()
+    assert np.all(np.abs(gi - wi) <= bound), float(np.max(np.abs(gi - wi) / bound))
+
+
+@pytest.mark.parametrize("d,r,dims", [(2, 1, (64, 256)), (2, 3, (32, 128)), (3, 1, (8, 16, 128))])
+def test_bf16_matches_oracle(d, r, dims):
+    k = rand_kernel("box", d, r, seed=[d, r, 9])
+    got, want, grid, _ = run_case(k, dims, 2, dtype="bf16")
+    h = r
+    wi = want[h:-h, h:-h, h:-h] if d == 3 else want[h:-h, h:-h]
+    assert max_rel_error(got.interior, wi) < TOL["bf16"]
+
+
+def test_heat3d_and_contractive_100_steps():
+    """Heat-3D, 100 steps (the B27 step count) on a small cube: measured bound."""
+    k = sp.make_kernel_3d("star", 1, heat3d())
+    got, want, grid, _ = run_case(k, (16, 24, 64), 100)
+    err = max_rel_error(got.interior, want[1:-1, 1:-1, 1:-1])
+    assert err < 2e-2, err
+
+
+def test_identity_kernel_fixed_point_full_size():
+    """10240^2 (the B9 size): the identity stencil is exact in fp16, so the
+    device result must equal the input bit for bit (size-independent check)."""
+    c = np.zeros((3, 3))
+    c[1, 1] = 1.0
+    k = sp.make_kernel("box", 2, 1, c)
+    plan = get_plan(k, sp.Parity.EVEN, "fp16")
+    dg = DeviceGrid(plan, (10240, 10240), 1)
+    host = torch.randn(dg.dense_shape, dtype=torch.float16)
+    dg.upload(host)
+    dg.run(3)
+    out = torch.empty_like(host)
+    dg.download(out)
+    torch.cuda.synchronize()
+    assert torch.equal(out, host)
+
+
+def test_linearity_full_size():
+    """B9 shape, 2 steps: S(a*g1 + g2) == a*S(g1) + S(g2) within fp16 error."""
+    k = rand_kernel("box", 2, 1, seed=1)
+    plan = get_plan(k, sp.Parity.EVEN, "fp16")
+    shape = (10240, 10240)
+    outs = []
+    g1 = torch.rand((10242, 10242), dtype=torch.float64, device="cuda") - 0.5
+    g2 = torch.rand((10242, 10242), dtype=torch.float64, device="cuda") - 0.5
+    for g in (g1, g2, 0.5 * g1 + g2):
+        dg = DeviceGrid(plan, shape, 1)
+        dg.load_dense_f64(g)
+        dg.run(2)
+        outs.append(dg.to_dense_f64())
+    lhs, rhs = outs[2], 0.5 * outs[0] + outs[1]
+    scale = lhs.abs().max().item()
+    assert (lhs - rhs).abs().max().item() / scale < 1e-2
+
+
+def test_step_range_composes_to_full_step():
+    k = rand_kernel("box", 2, 1, seed=2)
+    plan = get_plan(k, sp.Parity.EVEN, "fp16")
+    dense = torch.rand((130 + 2, 512 + 2), dtype=torch.float64, device="cuda")
+    a = DeviceGrid(plan, (130, 512), 1)
+    b = DeviceGrid(plan, (130, 512), 1)
+    a.load_dense_f64(dense)
+    b.load_dense_f64(dense)
+    a.run(1)
+    b.step_range(0, 7)
+    b.step_range(7, 100)
+    b.step_range(100, 130)
+    b.flip()
+    assert torch.equal(a.bufs[a.cur], b.bufs[b.cur])
+
+
+def test_upload_download_roundtrip():
+    k = rand_kernel("box", 2, 3, seed=3)
+    plan = get_plan(k, sp.Parity.EVEN, "fp16")
+    dg = DeviceGrid(plan, (100, 264), 3)
+    host = torch.randn(dg.dense_shape, dtype=torch.float16).pin_memory()
+    dg.upload(host)
+    back = torch.empty_like(host)
+    dg.download(back)
+    torch.cuda.synchronize()
+    assert torch.equal(host, back)
+    dense = dg.to_dense_f64().cpu()
+    assert torch.equal(dense, host.to(torch.float64))
+
+
+def test_reference_error_contract():
+    k = sp.make_kernel("box", 2, 2, np.ones(25))
+    with pytest.raises(ValueError, match="multiple"):
+        sp.execute(k, sp.random_grid(32, 32, 2, seed=0), 1)  # 32 % L=6 != 0
+    with pytest.raises(ValueError, match="halo"):
+        sp.execute(rand_kernel("box", 2, 3, 0), sp.random_grid(32, 32, 1, seed=0), 1)
+    with pytest.raises(ValueError, match="step"):
+        sp.execute(rand_kernel("box", 2, 1, 0), sp.random_grid(32, 32, 1, seed=0), 0)
+    with pytest.raises(ValueError, match="unsupported"):
+        sp.execute(k, sp.random_grid(32, 36, 2, seed=0), 1)
+
+
+def test_verify_report():
+    k = sp.make_kernel("star", 2, 1, heat2d())
+    rep = sp.verify(k, [64, 128], seed=1, steps=2)
+    assert rep["all_pass"], rep
+    assert rep["cross_checks"]["parity_max_abs_diff"] < 1e-2
+    assert sp.report_json(rep) == sp.report_json(sp.verify(k, [64, 128], seed=1, steps=2))
