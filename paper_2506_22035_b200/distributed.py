@@ -1,0 +1,191 @@
+"""Multi-GPU slab driver: domain decomposition with one halo exchange per step.
+
+The reference has no distribution; per SURVEY.md §8(e) the
+grid is cut into contiguous slabs along the slowest axis (y in 2D, z in 3D),
+one rank per GPU.  Each step:
+
+  1. the two boundary tile bands of the slab are computed first
+     (compute stream);
+  2. their r outermost rows are packed and exchanged with the y-1 / y+1 ranks
+     by NCCL send/recv on a communication stream, then unpacked into the halo
+     rows of the freshly written buffer — overlapped with
+  3. the interior bands (compute stream);
+  4. the compute stream waits for the exchange before the next step reads the
+     halos.
+
+Outer ranks keep the global Dirichlet halo.  The orchestration is written
+against `SlabOps` so the exchange logic is tested with gloo on CPU
+(tests/test_distributed.py) while the device ops call libspider.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from ._lib import check, lib
+from .engine import DeviceGrid, Plan, _stream_ptr
+
+
+@dataclass(frozen=True)
+class Slab:
+    """Rows [lo, hi) of a global extent owned by `rank` of `world`."""
+
+    rank: int
+    world: int
+    lo: int
+    hi: int
+
+    @property
+    def rows(self) -> int:
+        return self.hi - self.lo
+
+    @property
+    def up(self) -> int | None:
+        return self.rank - 1 if self.rank > 0 else None
+
+    @property
+    def down(self) -> int | None:
+        return self.rank + 1 if self.rank < self.world - 1 else None
+
+
+def decompose(global_rows: int, world: int, rank: int, align: int = 1) -> Slab:
+    """Contiguous split; slab boundaries are multiples of `align` (the tile
+    height) except the last, so boundary bands are whole tiles."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    units = -(-global_rows // align)
+    if units < world:
+        raise ValueError(f"{global_rows} rows cannot be split into {world} slabs of {align}-row tiles")
+    lo = (units * rank // world) * align
+    hi = min(global_rows, (units * (rank + 1) // world) * align)
+    return Slab(rank, world, lo, hi)
+
+
+def exchange(slab: Slab, send_up, send_down, recv_up, recv_down, group=None) -> None:
+    """Post the neighbour sends/receives of one step and wait for them.
+    Works on CUDA tensors (NCCL) and CPU tensors (gloo)."""
+    ops = []
+    if slab.up is not None:
+        ops.append(dist.P2POp(dist.isend, send_up, slab.up, group))
+        ops.append(dist.P2POp(dist.irecv, recv_up, slab.up, group))
+    if slab.down is not None:
+        ops.append(dist.P2POp(dist.isend, send_down, slab.down, group))
+        ops.append(dist.P2POp(dist.irecv, recv_down, slab.down, group))
+    if not ops:
+        return
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+
+
+class SlabOps:
+    """What the driver needs from a local slab (device or test double)."""
+
+    r: int
+    rows: int
+    band: int
+
+    def compute(self, lo: int, hi: int) -> None:  # one step over local rows [lo, hi)
+        raise NotImplementedError
+
+    def flip(self) -> None:
+        raise NotImplementedError
+
+    def pack(self, which: str, msg) -> None:  # 'up': rows [0, r); 'down': rows [rows-r, rows)
+        raise NotImplementedError
+
+    def unpack(self, which: str, msg) -> None:  # 'up': halo rows [-r, 0); 'down': [rows, rows+r)
+        raise NotImplementedError
+
+    def new_message(self):
+        raise NotImplementedError
+
+
+class SlabDriver:
+    """Runs steps of a slab with boundary-first compute and overlapped exchange."""
+
+    def __init__(self, slab: Slab, ops: SlabOps, group=None, comm_stream=None, compute_stream=None):
+        self.slab, self.ops, self.group = slab, ops, group
+        self.msgs = {k: ops.new_message() for k in ("send_up", "send_down", "recv_up", "recv_down")}
+        self.comm_stream = comm_stream
+        self.compute_stream = compute_stream
+
+    def _bands(self):
+        rows, band = self.ops.rows, self.ops.band
+        if rows <= 2 * band:
+            return [(0, rows)], []
+        return [(0, band), (rows - band, rows)], [(band, rows - band)]
+
+    def step(self) -> None:
+        boundary, interior = self._bands()
+        cuda = self.comm_stream is not None
+        for lo, hi in boundary:
+            self.ops.compute(lo, hi)
+        if cuda:
+            done = torch.cuda.Event()
+            done.record(self.compute_stream)
+            with torch.cuda.stream(self.comm_stream):
+                self.comm_stream.wait_event(done)
+                self._exchange()
+                exchanged = torch.cuda.Event()
+                exchanged.record(self.comm_stream)
+            for lo, hi in interior:
+                self.ops.compute(lo, hi)
+            self.compute_stream.wait_event(exchanged)
+        else:
+            self._exchange()
+            for lo, hi in interior:
+                self.ops.compute(lo, hi)
+        self.ops.flip()
+
+    def _exchange(self) -> None:
+        m, s = self.msgs, self.slab
+        if s.up is not None:
+            self.ops.pack("up", m["send_up"])
+        if s.down is not None:
+            self.ops.pack("down", m["send_down"])
+        exchange(s, m["send_up"], m["send_down"], m["recv_up"], m["recv_down"], self.group)
+        if s.up is not None:
+            self.ops.unpack("up", m["recv_up"])
+        if s.down is not None:
+            self.ops.unpack("down", m["recv_down"])
+
+
+class DeviceSlabOps(SlabOps):
+    """libspider-backed slab: a DeviceGrid whose halo rows at inner slab faces
+    are refreshed by the exchange (outer faces keep the global Dirichlet halo)."""
+
+    def __init__(self, plan: Plan, local_shape, halo: int, stream=None):
+        self.grid = DeviceGrid(plan, local_shape, halo)
+        self.plan = plan
+        self.r = plan.kernel.r
+        self.rows = int(local_shape[0])
+        self.band = plan.info().tile_z if plan.kernel.d == 3 else plan.info().tile_y
+        self.stream = stream
+        d = self.grid.desc
+        self.unit = d.plane if plan.kernel.d == 3 else d.pitch
+
+    def compute(self, lo: int, hi: int) -> None:
+        self.grid.step_range(lo, hi, self.stream)
+
+    def flip(self) -> None:
+        self.grid.flip()
+
+    def new_message(self):
+        return torch.empty(self.r * self.unit, dtype=self.grid.bufs[0].dtype, device=self.grid.bufs[0].device)
+
+    def _out(self):
+        return self.grid.bufs[1 - self.grid.cur]  # buffer being written this step
+
+    def pack(self, which: str, msg) -> None:
+        check(lib.spd_halo_pack(C.byref(self.grid.desc), C.c_void_p(self._out().data_ptr()), self.r,
+                                0 if which == "up" else 1, C.c_void_p(msg.data_ptr()), _stream_ptr()))
+
+    def unpack(self, which: str, msg) -> None:
+        check(lib.spd_halo_unpack(C.byref(self.grid.desc), C.c_void_p(self._out().data_ptr()), self.r,
+                                  0 if which == "up" else 1, C.c_void_p(msg.data_ptr()), _stream_ptr()))
+
+
+__all__ = ["Slab", "decompose", "exchange", "SlabOps", "SlabDriver", "DeviceSlabOps"]

@@ -231,11 +231,17 @@ def _stats(kernel: StencilKernel, grid, steps: int, parity: Parity, plan: Plan) 
     return st
 
 
-def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig()):
+def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=None):
     """Run `steps` steps on the B200 sparse-tensor-core path; returns
     (Grid, ExecStats) like reference pipeline.py:189-262.  The input grid is
-    never modified.  float16 host grids are transferred as-is (pinned host
-    memory gives asynchronous DMA); other dtypes are quantised on the device.
+    never modified.
+
+    float16 host grids are transferred as-is by strided DMA (pinned host memory
+    gives asynchronous copies) and the result comes back as float16, into
+    `out.data` when an `out` grid of the same shape is given (otherwise into a
+    pinned buffer from torch's caching host allocator).  Other dtypes are
+    quantised on the device and the result is returned as float64 (float32
+    inputs give float32).
     """
     _check_inputs(kernel, grid, steps)
     dcfg = _device_cfg(cfg)
@@ -250,14 +256,22 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig()):
         dg.load_dense_f64(torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dg.bufs[0].device))
     dg.run(steps)
     if native16:
-        out = torch.empty(dg.dense_shape, dtype=torch.float16)
-        dg.download(out)
+        if out is not None:
+            if out.data.shape != data.shape or out.data.dtype != np.float16 or not out.data.flags.c_contiguous:
+                raise ValueError("out grid must be a contiguous float16 array of the input's shape")
+            target = torch.from_numpy(out.data)
+        else:
+            target = torch.empty(dg.dense_shape, dtype=torch.float16, pin_memory=True)
+        dg.download(target)
         torch.cuda.current_stream().synchronize()
-        res = out.numpy()
+        res = target.numpy()
     else:
         res = dg.to_dense_f64().cpu().numpy()
-        if data.dtype in (np.float32,):
+        if data.dtype == np.float32:
             res = res.astype(np.float32)
+        if out is not None:
+            out.data[...] = res
+            res = out.data
     cls = Grid3D if kernel.d == 3 else Grid
     return cls(res, grid.halo, grid.step + steps), _stats(kernel, grid, steps, dcfg.parity, plan)
 
