@@ -290,98 +290,120 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     // ===================== producer: natural rows -> permuted B image =====
     const int pw = warp - kEpiWarps;
     const int n_items = g.r_in * C::SEGS;
+    constexpr int R = (L - 2) / 2;
+    // ext[] words actually referenced by the windows (compile time):
+    //   element e of ext is x = 8*lane - 8 + e; windows span
+    //   e in [8 - R, 8 + (CPL-1)*L - R + 2L - 1]
+    constexpr int kPrevW = (8 - R) / 2;                                     // first prev word used
+    constexpr int kNextW = (8 + (C::CPL - 1) * L - R + 2 * L - 1) / 2 - 8;  // last next word used
+    // Loop-invariant per-item offsets (element offset of the segment start
+    // relative to the tile origin, and the lane's B-image byte offset).
+    int64_t goff[NQ];
+    uint32_t soff[NQ];
+    bool valid[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int item = pw + q * kProdWarps;
+      valid[q] = item < n_items;
+      const int b = valid[q] ? item / C::SEGS : 0, sg = valid[q] ? item % C::SEGS : 0;
+      goff[q] = (int64_t)g.in_dz[b] * p.plane + (int64_t)g.in_dy[b] * p.pitch + g.in_dx[b] + (int64_t)sg * 256;
+      const int n0 = sg * C::SEG + lane * C::CPL;
+      soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(n0 / 8) * sbo + (n0 % 8) * 16;
+    }
+    // CPL = 2: lanes 4-7 of a quarter-warp hit the next core-matrix group at
+    // the same bank offsets as lanes 0-3; they store their odd chunk first so
+    // every STS.128 phase covers the 32 banks once.
+    const bool flip = C::CPL == 2 && ((lane >> 2) & 1);
     int it = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
       const uint32_t sphase = (it / NSTAGE) & 1;
       int64_t z0, y0, x0;
       tile_origin(t, z0, y0, x0);
-      uint4 cur[NQ], edge[NQ];
+      const T* tbase = in + p.origin + z0 * p.plane + y0 * p.pitch + x0;
+      uint4 cur[NQ];
+      uint32_t ep[NQ][4 - kPrevW];  // lane 0: words kPrevW..3 of x - 8
+      uint32_t en[NQ][kNextW + 1];  // lane 31: words 0..kNextW of x + 256
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const int item = pw + q * kProdWarps;
-        if (item < n_items) {
-          const int b = item / C::SEGS, sg = item % C::SEGS;
-          const T* row = in + p.origin + (z0 + g.in_dz[b]) * p.plane + (y0 + g.in_dy[b]) * p.pitch +
-                         x0 + g.in_dx[b] + (int64_t)sg * 256;
+        if (valid[q]) {
+          const T* row = tbase + goff[q];
           cur[q] = __ldg(reinterpret_cast<const uint4*>(row) + lane);
-          if (lane == 0) edge[q] = __ldg(reinterpret_cast<const uint4*>(row) - 1);
-          if (lane == 31) edge[q] = __ldg(reinterpret_cast<const uint4*>(row) + 32);
+          if (lane == 0) {
+            const uint32_t* pe = reinterpret_cast<const uint32_t*>(row - 8) + kPrevW;
+            if (4 - kPrevW == 2) {
+              uint2 v = __ldg(reinterpret_cast<const uint2*>(pe));
+              ep[q][0] = v.x;
+              ep[q][(4 - kPrevW) - 1] = v.y;
+            } else {
+#pragma unroll
+              for (int w = 0; w < 4 - kPrevW; ++w) ep[q][w] = __ldg(pe + w);
+            }
+          }
+          if (lane == 31) {
+            const uint32_t* ne = reinterpret_cast<const uint32_t*>(row + 256);
+            if (kNextW + 1 == 2) {
+              uint2 v = __ldg(reinterpret_cast<const uint2*>(ne));
+              en[q][0] = v.x;
+              en[q][kNextW] = v.y;
+            } else {
+              uint4 v = __ldg(reinterpret_cast<const uint4*>(ne));
+              en[q][0] = v.x;
+              if (kNextW >= 1) en[q][kNextW >= 1 ? 1 : 0] = v.y;
+              if (kNextW >= 2) en[q][kNextW >= 2 ? 2 : 0] = v.z;
+              if (kNextW >= 3) en[q][kNextW >= 3 ? 3 : 0] = v.w;
+            }
+          }
         }
       }
       mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
       const uint32_t sbase = bimg_s + stage * stage_bytes;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const int item = pw + q * kProdWarps;
-        if (item < n_items) {
-          const int b = item / C::SEGS, sg = item % C::SEGS;
+        if (valid[q]) {
           uint32_t ext[12];
-          ext[4] = cur[q].x;
-          ext[5] = cur[q].y;
-          ext[6] = cur[q].z;
-          ext[7] = cur[q].w;
-          ext[0] = __shfl_up_sync(0xffffffffu, cur[q].x, 1);
-          ext[1] = __shfl_up_sync(0xffffffffu, cur[q].y, 1);
-          ext[2] = __shfl_up_sync(0xffffffffu, cur[q].z, 1);
-          ext[3] = __shfl_up_sync(0xffffffffu, cur[q].w, 1);
-          ext[8] = __shfl_down_sync(0xffffffffu, cur[q].x, 1);
-          ext[9] = __shfl_down_sync(0xffffffffu, cur[q].y, 1);
-          ext[10] = __shfl_down_sync(0xffffffffu, cur[q].z, 1);
-          ext[11] = __shfl_down_sync(0xffffffffu, cur[q].w, 1);
-          if (lane == 0) {
-            ext[0] = edge[q].x;
-            ext[1] = edge[q].y;
-            ext[2] = edge[q].z;
-            ext[3] = edge[q].w;
+          const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) ext[4 + w] = cw[w];
+#pragma unroll
+          for (int w = kPrevW; w < 4; ++w) {
+            ext[w] = __shfl_up_sync(0xffffffffu, cw[w], 1);
+            if (lane == 0) ext[w] = ep[q][w - kPrevW];
           }
-          if (lane == 31) {
-            ext[8] = edge[q].x;
-            ext[9] = edge[q].y;
-            ext[10] = edge[q].z;
-            ext[11] = edge[q].w;
+#pragma unroll
+          for (int w = 0; w <= kNextW; ++w) {
+            ext[8 + w] = __shfl_down_sync(0xffffffffu, cw[w], 1);
+            if (lane == 31) ext[8 + w] = en[q][w];
           }
-          uint32_t w[C::CPL][KC][4];
+          uint32_t wd[C::CPL][KC][4];
 #pragma unroll
           for (int c = 0; c < C::CPL; ++c)
 #pragma unroll
             for (int kc = 0; kc < KC; ++kc)
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                // element index in ext (16-bit units): x = 8*lane - 8 + e
-                constexpr int R = (L - 2) / 2;
                 const int e0 = 8 + c * L - R + perm_slot(L, PARITY, 8 * kc + 2 * u);
                 const int e1 = 8 + c * L - R + perm_slot(L, PARITY, 8 * kc + 2 * u + 1);
-                w[c][kc][u] = __byte_perm(ext[e0 / 2], ext[e1 / 2], sel_halves(e0 % 2, e1 % 2));
+                wd[c][kc][u] = __byte_perm(ext[e0 / 2], ext[e1 / 2], sel_halves(e0 % 2, e1 % 2));
               }
-          const int n0 = sg * C::SEG + lane * C::CPL;  // first chunk of this lane
+          const uint32_t a0 = sbase + soff[q];
           if (C::CPL == 2) {
-            // Lanes 4-7 of each quarter-warp write the next core-matrix group at
-            // the same bank offsets as lanes 0-3: store their odd chunk first so
-            // every STS.128 phase covers all 32 banks once.
-            const bool flip = (lane >> 2) & 1;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-              const int n = n0 + (c ^ (int)flip);
-              const uint32_t gbase = sbase + (n / 8) * sbo + (n % 8) * 16 + b * KC * 128;
+              const int ci = c ^ (int)flip;
+              const uint32_t addr = a0 + (ci ? 16u : 0u);  // chunks n0, n0+1: adjacent core-matrix rows
 #pragma unroll
               for (int kc = 0; kc < KC; ++kc) {
-                const int ci = c ^ (int)flip;
-                uint32_t a0 = ci ? w[C::CPL - 1][kc][0] : w[0][kc][0];
-                uint32_t a1 = ci ? w[C::CPL - 1][kc][1] : w[0][kc][1];
-                uint32_t a2 = ci ? w[C::CPL - 1][kc][2] : w[0][kc][2];
-                uint32_t a3 = ci ? w[C::CPL - 1][kc][3] : w[0][kc][3];
-                sts_v4(gbase + kc * 128, a0, a1, a2, a3);
+                const uint32_t v0 = ci ? wd[C::CPL - 1][kc][0] : wd[0][kc][0];
+                const uint32_t v1 = ci ? wd[C::CPL - 1][kc][1] : wd[0][kc][1];
+                const uint32_t v2 = ci ? wd[C::CPL - 1][kc][2] : wd[0][kc][2];
+                const uint32_t v3 = ci ? wd[C::CPL - 1][kc][3] : wd[0][kc][3];
+                sts_v4(addr + kc * 128, v0, v1, v2, v3);
               }
             }
           } else {
 #pragma unroll
-            for (int c = 0; c < C::CPL; ++c) {
-              const int n = n0 + c;
-              const uint32_t gbase = sbase + (n / 8) * sbo + (n % 8) * 16 + b * KC * 128;
-#pragma unroll
-              for (int kc = 0; kc < KC; ++kc) sts_v4(gbase + kc * 128, w[c][kc][0], w[c][kc][1], w[c][kc][2], w[c][kc][3]);
-            }
+            for (int kc = 0; kc < KC; ++kc) sts_v4(a0 + kc * 128, wd[0][kc][0], wd[0][kc][1], wd[0][kc][2], wd[0][kc][3]);
           }
         }
       }
@@ -404,9 +426,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       if (lane == 0) {
         const uint32_t sbase = bimg_s + stage * stage_bytes;
         const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
-        for (int s = 0; s < g.s; ++s) {
-          const uint64_t bdesc = umma_desc(sbase + g.start_row[s] * KC * 128, 128, sbo);
-          mma_sp_ts(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
+#pragma unroll
+        for (int s = 0; s < SPD_MAX_S; ++s) {
+          if (s < g.s) {
+            const uint64_t bdesc = umma_desc(sbase + g.start_row[s] * KC * 128, 128, sbo);
+            mma_sp_ts(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
+          }
         }
         tc_commit(bar_empty + 8 * stage);
         tc_commit(bar_accf + 8 * acc);
@@ -419,15 +444,16 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const int alpha = m / L;              // output row of the tile
     const int d = lane % L;               // position in the L-lane group
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
     int it = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
       const int acc = it % NACC;
       const uint32_t aphase = (it / NACC) & 1;
       int64_t z0, y0, x0;
       tile_origin(t, z0, y0, x0);
-      const int64_t z = z0 + g.out_dz[alpha];
-      const int64_t y = y0 + g.out_dy[alpha];
-      const int64_t xr = x0 + g.out_dx[alpha];  // x of chunk 0 of this row
+      const int64_t z = z0 + odz;
+      const int64_t y = y0 + ody;
+      const int64_t xr = x0 + odx;  // x of chunk 0 of this row
       bool row_ok;
       if (g.d == 3) row_ok = z >= p.row_lo && z < p.row_hi && y < p.ny;
       else if (g.d == 2) row_ok = y >= p.row_lo && y < p.row_hi;
