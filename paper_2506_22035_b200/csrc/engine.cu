@@ -16,6 +16,7 @@
 //   warp 12    MMA      : one thread issues S tcgen05.mma.sp per tile with the
 //                         compressed kernel (A) and metadata (E) resident in
 //                         TMEM for the whole launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
@@ -167,7 +168,12 @@ __host__ __device__ constexpr uint32_t sel_halves(int ha, int hb) {
 // Kernel parameters
 
 struct StepParams {
+  CUtensorMap tmap;          // input grid as a 2D / 3D tensor (tensor-TMA mode)
   Geometry g;
+  int use_tmap;              // 1: tensor-TMA boxes, 0: 1D bulk copies per row
+  int nbox, boxw, box_slot;  // natural-stage layout: [box][row][boxw] elements
+  int nat_bytes;             // bytes per natural stage
+  int xoff, yoff, zoff;      // stored coordinates of interior (0, 0, 0)
   const void* in;
   void* out;
   int64_t pitch, plane, origin;
@@ -183,15 +189,19 @@ struct StepParams {
 
 constexpr int kEpiWarps = 4;
 constexpr int kProdWarps = 8;
-constexpr int kThreads = 32 * (kEpiWarps + kProdWarps + 1);
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+constexpr int kLoadWarp = kMmaWarp + 1;
+constexpr int kThreads = 32 * (kLoadWarp + 1);
 
-template <int L, int NTILE, int NSTAGE, int NACC, int NQ>
+template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
 struct Cfg {
   static constexpr int KC = 2 * L / 8;
-  static constexpr int CPL = 8 / L;          // chunks per lane per 16-B load
-  static constexpr int SEG = 32 * CPL;       // chunks per warp segment
+  static constexpr int CPL = 8 / L;          // chunks per lane per 16-B word group
+  static constexpr int SEG = 32 * CPL;       // chunks per warp segment (256 points)
   static constexpr int SEGS = NTILE / SEG;   // segments per tile row
+  // natural row segment staged by the bulk copy: [x0 - 8, x0 + NTILE*L + 8)
+  static constexpr int ROW_ELEMS = NTILE * L + 16;
+  static constexpr int ROW_BYTES = ROW_ELEMS * 2;
   static constexpr int ACC_COL = 0;
   static constexpr int E_COL = NACC * NTILE;
   // E for MMA s at E_COL + 2s: bit 0 of the metadata TMEM address is the
@@ -201,26 +211,72 @@ struct Cfg {
   static_assert(NTILE % SEG == 0, "tile width must be whole warp segments");
 };
 
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 
+// 1D bulk copy global -> shared on the TMA engine, completing on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// Tensor TMA box loads (tile mode, no swizzle), completing on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // The stencil step kernel.
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NACC, int NQ>
+//
+// Pipelines (all mbarrier based):
+//   loader --(nat_full: tx bytes)--> producers --(nat_empty)--> loader
+//   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
+//   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
 __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
-  using C = Cfg<L, NTILE, NSTAGE, NACC, NQ>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, NQ>;
   constexpr int KC = C::KC;
   const Geometry& g = p.g;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int sbo = g.b_sbo;
   const int stage_bytes = (NTILE / 8) * sbo;
   uint8_t* bimg = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NSTAGE * stage_bytes);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC);
+  uint8_t* nat = smem + NSTAGE * stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(nat + NNAT * p.nat_bytes);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC + 2 * NNAT);
   const uint32_t bimg_s = smem_u32(bimg);
+  const uint32_t nat_s = smem_u32(nat);
   const uint32_t bar_full = smem_u32(bars);
   const uint32_t bar_empty = bar_full + 8 * NSTAGE;
   const uint32_t bar_accf = bar_full + 16 * NSTAGE;
   const uint32_t bar_acce = bar_accf + 8 * NACC;
+  const uint32_t bar_natf = bar_acce + 8 * NACC;
+  const uint32_t bar_nate = bar_natf + 8 * NNAT;
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -234,11 +290,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       mbar_init(bar_accf + 8 * a, 1);
       mbar_init(bar_acce + 8 * a, kEpiWarps);
     }
+    for (int a = 0; a < NNAT; ++a) {
+      mbar_init(bar_natf + 8 * a, 1);
+      mbar_init(bar_nate + 8 * a, kProdWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(tmem_holder)),
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                  "n"(C::TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -286,7 +345,42 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     z0 = (int64_t)(p.tile_z0 + bz) * g.tile_z;
   };
 
-  if (warp >= kEpiWarps && warp < kMmaWarp) {
+  if (warp == kLoadWarp) {
+    // ===================== loader: TMA copies of the natural input rows ===
+    // 2D/3D: the tile's halo-padded input block as nbox tensor boxes
+    // (cp.async.bulk.tensor); 1D: one bulk copy per line segment.
+    if (lane == 0) {
+      const uint32_t box_bytes = (uint32_t)(p.boxw * 2 * g.r_in);
+      int it = 0;
+      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+        const int ns = it % NNAT;
+        const uint32_t nphase = (it / NNAT) & 1;
+        int64_t z0, y0, x0;
+        tile_origin(t, z0, y0, x0);
+        mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
+        const uint32_t dst = nat_s + ns * p.nat_bytes;
+        const uint32_t fb = bar_natf + 8 * ns;
+        if (p.use_tmap) {
+          mbar_arrive_expect_tx(fb, box_bytes * p.nbox);
+          const int c0 = (int)(p.xoff + x0 - 8);
+          const int c1 = (int)(p.yoff + y0 - g.r);
+          if (g.d == 3) {
+            const int c2 = (int)(p.zoff + z0 - g.r);
+            for (int k = 0; k < p.nbox; ++k) tma_load_3d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, c2, fb);
+          } else {
+            for (int k = 0; k < p.nbox; ++k) tma_load_2d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, fb);
+          }
+        } else {
+          mbar_arrive_expect_tx(fb, (uint32_t)(g.r_in * C::ROW_BYTES));
+          const T* tbase = in + p.origin + z0 * p.plane + y0 * p.pitch + x0 - 8;
+          for (int b = 0; b < g.r_in; ++b) {
+            const T* src = tbase + (int64_t)g.in_dz[b] * p.plane + (int64_t)g.in_dy[b] * p.pitch + g.in_dx[b];
+            bulk_g2s(dst + b * C::ROW_BYTES, src, C::ROW_BYTES, fb);
+          }
+        }
+      }
+    }
+  } else if (warp >= kEpiWarps && warp < kMmaWarp) {
     // ===================== producer: natural rows -> permuted B image =====
     const int pw = warp - kEpiWarps;
     const int n_items = g.r_in * C::SEGS;
@@ -296,17 +390,24 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     //   e in [8 - R, 8 + (CPL-1)*L - R + 2L - 1]
     constexpr int kPrevW = (8 - R) / 2;                                     // first prev word used
     constexpr int kNextW = (8 + (C::CPL - 1) * L - R + 2 * L - 1) / 2 - 8;  // last next word used
-    // Loop-invariant per-item offsets (element offset of the segment start
-    // relative to the tile origin, and the lane's B-image byte offset).
-    int64_t goff[NQ];
-    uint32_t soff[NQ];
+    // Loop-invariant per-item offsets: natural-stage byte offset of the lane's
+    // 16 B and the lane's B-image byte offset.
+    uint32_t noff[NQ], poff[NQ], xoff_n[NQ], soff[NQ];
     bool valid[NQ];
+    // natural stage: element x of row b at box k = x / boxw
+    auto nat_addr = [&](int b, int x) -> uint32_t {
+      const int k = x / p.boxw;
+      return (uint32_t)(k * p.box_slot + (b * p.boxw + (x - k * p.boxw)) * 2);
+    };
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int item = pw + q * kProdWarps;
       valid[q] = item < n_items;
       const int b = valid[q] ? item / C::SEGS : 0, sg = valid[q] ? item % C::SEGS : 0;
-      goff[q] = (int64_t)g.in_dz[b] * p.plane + (int64_t)g.in_dy[b] * p.pitch + g.in_dx[b] + (int64_t)sg * 256;
+      const int xl = 8 + sg * 256 + lane * 8;  // this lane's 8 points (stage-local x)
+      noff[q] = nat_addr(b, xl);
+      poff[q] = nat_addr(b, xl - 8);
+      xoff_n[q] = nat_addr(b, xl + 8);
       const int n0 = sg * C::SEG + lane * C::CPL;
       soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(n0 / 8) * sbo + (n0 % 8) * 16;
     }
@@ -318,62 +419,29 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
       const uint32_t sphase = (it / NSTAGE) & 1;
-      int64_t z0, y0, x0;
-      tile_origin(t, z0, y0, x0);
-      const T* tbase = in + p.origin + z0 * p.plane + y0 * p.pitch + x0;
-      uint4 cur[NQ];
-      uint32_t ep[NQ][4 - kPrevW];  // lane 0: words kPrevW..3 of x - 8
-      uint32_t en[NQ][kNextW + 1];  // lane 31: words 0..kNextW of x + 256
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        if (valid[q]) {
-          const T* row = tbase + goff[q];
-          cur[q] = __ldg(reinterpret_cast<const uint4*>(row) + lane);
-          if (lane == 0) {
-            const uint32_t* pe = reinterpret_cast<const uint32_t*>(row - 8) + kPrevW;
-            if (4 - kPrevW == 2) {
-              uint2 v = __ldg(reinterpret_cast<const uint2*>(pe));
-              ep[q][0] = v.x;
-              ep[q][(4 - kPrevW) - 1] = v.y;
-            } else {
-#pragma unroll
-              for (int w = 0; w < 4 - kPrevW; ++w) ep[q][w] = __ldg(pe + w);
-            }
-          }
-          if (lane == 31) {
-            const uint32_t* ne = reinterpret_cast<const uint32_t*>(row + 256);
-            if (kNextW + 1 == 2) {
-              uint2 v = __ldg(reinterpret_cast<const uint2*>(ne));
-              en[q][0] = v.x;
-              en[q][kNextW] = v.y;
-            } else {
-              uint4 v = __ldg(reinterpret_cast<const uint4*>(ne));
-              en[q][0] = v.x;
-              if (kNextW >= 1) en[q][kNextW >= 1 ? 1 : 0] = v.y;
-              if (kNextW >= 2) en[q][kNextW >= 2 ? 2 : 0] = v.z;
-              if (kNextW >= 3) en[q][kNextW >= 3 ? 3 : 0] = v.w;
-            }
-          }
-        }
-      }
+      const int ns = it % NNAT;
+      const uint32_t nphase = (it / NNAT) & 1;
+      const uint32_t nbase = nat_s + ns * p.nat_bytes;
+      mbar_wait(bar_natf + 8 * ns, nphase);
       mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
       const uint32_t sbase = bimg_s + stage * stage_bytes;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         if (valid[q]) {
+          const uint4 cur = lds_v4(nbase + noff[q]);
           uint32_t ext[12];
-          const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
+          const uint32_t cw[4] = {cur.x, cur.y, cur.z, cur.w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) ext[4 + w] = cw[w];
 #pragma unroll
           for (int w = kPrevW; w < 4; ++w) {
             ext[w] = __shfl_up_sync(0xffffffffu, cw[w], 1);
-            if (lane == 0) ext[w] = ep[q][w - kPrevW];
+            if (lane == 0) ext[w] = lds_u32(nbase + poff[q] + 4 * w);
           }
 #pragma unroll
           for (int w = 0; w <= kNextW; ++w) {
             ext[8 + w] = __shfl_down_sync(0xffffffffu, cw[w], 1);
-            if (lane == 31) ext[8 + w] = en[q][w];
+            if (lane == 31) ext[8 + w] = lds_u32(nbase + xoff_n[q] + 4 * w);
           }
           uint32_t wd[C::CPL][KC][4];
 #pragma unroll
@@ -409,7 +477,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar_full + 8 * stage);
+      if (lane == 0) {
+        mbar_arrive(bar_nate + 8 * ns);
+        mbar_arrive(bar_full + 8 * stage);
+      }
     }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer ======================================
@@ -440,9 +511,9 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
   } else {
     // ===================== epilogue ========================================
-    const int m = warp * 32 + lane;       // TMEM lane == M row
-    const int alpha = m / L;              // output row of the tile
-    const int d = lane % L;               // position in the L-lane group
+    const int m = warp * 32 + lane;  // TMEM lane == M row
+    const int alpha = m / L;         // output row of the tile
+    const int d = lane % L;          // position in the L-lane group
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
     const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
     int it = 0;
@@ -708,20 +779,28 @@ struct spd_plan {
 
 namespace spd {
 
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NACC, int NQ>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NACC, NQ>;
-  const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + 8 * (2 * NSTAGE + 2 * NACC) + 16;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, NQ>;
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, NQ>;
+  sp.nat_bytes = sp.use_tmap ? sp.nbox * sp.box_slot : plan->g.r_in * C::ROW_BYTES;
+  if (!sp.use_tmap) {
+    sp.nbox = 1;
+    sp.boxw = C::ROW_ELEMS;
+    sp.box_slot = sp.nat_bytes;
+  }
+  const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + (size_t)NNAT * sp.nat_bytes +
+                      8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT) + 16;
+  if (smem > 232448) return set_error(SPD_EUNSUPPORTED, "shared memory budget exceeded (%zu B)", smem);
+  if (C::A_COL + 8 * plan->g.s > 512) return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
   static thread_local int configured_dev = -1;
-  // cudaFuncSetAttribute is per function; cheap enough to call each time on
-  // a new device, cache per thread otherwise.
-  if (configured_dev != plan->device) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static thread_local size_t configured_smem = 0;
+  if (configured_dev != plan->device || configured_smem < smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
     configured_dev = plan->device;
+    configured_smem = 232448;
   }
-  if (Cfg<L, NTILE, NSTAGE, NACC, NQ>::A_COL + 8 * plan->g.s > 512)
-    return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
   if (sp.n_tiles <= 0) return SPD_OK;
   int grid = sp.n_tiles < plan->sms ? sp.n_tiles : plan->sms;
   kern<<<grid, kThreads, smem, stream>>>(sp);
@@ -734,15 +813,15 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   // items per producer warp: ceil(r_in * segs / 8)
   if (g.L == 4 && g.n_tile == 128) {
     // 2D (r_in 34, 2 segs -> 68 items) and 1D (r_in 32 -> 64 items)
-    return launch_step<T, 4, PARITY, 128, 3, 3, 9>(plan, sp, st);
+    return launch_step<T, 4, PARITY, 128, 1, 4, 3, 9>(plan, sp, st);
   }
   if (g.L == 4 && g.n_tile == 64) {
     // 3D: r_in 60, 1 seg -> 60 items
-    return launch_step<T, 4, PARITY, 64, 3, 4, 8>(plan, sp, st);
+    return launch_step<T, 4, PARITY, 64, 1, 5, 4, 8>(plan, sp, st);
   }
   if (g.L == 8 && g.n_tile == 64) {
     // 2D r=3: r_in 22, 2 segs -> 44 items; 1D: 16 rows -> 32 items
-    return launch_step<T, 8, PARITY, 64, 4, 4, 6>(plan, sp, st);
+    return launch_step<T, 8, PARITY, 64, 2, 5, 4, 6>(plan, sp, st);
   }
   return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
 }
@@ -755,6 +834,49 @@ static int dispatch(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
 }
 
 static int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  });
+  return fn;
+}
+
+// Tensor map of an input buffer for the loader warp: the stored grid as a
+// [planes][rows][pitch] (3D) or [rows][pitch] (2D) tensor of 16-bit elements;
+// one box = nbox-th of the tile's halo-padded input block.
+static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const void* buf, StepParams& sp) {
+  const Geometry& g = plan->g;
+  const int row_elems = g.n_tile * g.L + 16;
+  sp.nbox = (row_elems + 255) / 256;
+  sp.boxw = row_elems / sp.nbox;
+  if (row_elems % sp.nbox || sp.boxw % 8) return set_error(SPD_EUNSUPPORTED, "bad TMA box split (%d)", row_elems);
+  sp.box_slot = (int)roundup((int64_t)sp.boxw * 2 * g.r_in, 128);
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const int64_t rows = gd->plane / gd->pitch;
+  cuuint64_t dims[3] = {(cuuint64_t)gd->pitch, (cuuint64_t)rows, (cuuint64_t)(gd->alloc_elems / gd->plane)};
+  cuuint64_t strides[2] = {(cuuint64_t)gd->pitch * 2, (cuuint64_t)gd->plane * 2};
+  cuuint32_t box[3] = {(cuuint32_t)sp.boxw, (cuuint32_t)(g.tile_y + 2 * g.r), (cuuint32_t)(g.tile_z + 2 * g.r)};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const cuuint32_t rank = g.d == 3 ? 3 : 2;
+  CUresult r = enc(&sp.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, rank, const_cast<void*>(buf), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  sp.use_tmap = 1;
+  return SPD_OK;
+}
 
 static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int64_t lo,
                             int64_t hi, StepParams& sp) {
@@ -795,6 +917,11 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     sp.tiles_y = sp.tiles_z = 1;
   }
   sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
+  sp.zoff = (int)(gd->origin / gd->plane);
+  sp.yoff = (int)((gd->origin % gd->plane) / gd->pitch);
+  sp.xoff = (int)(gd->origin % gd->pitch);
+  sp.use_tmap = 0;
+  if (g.d >= 2) return make_tensor_map(plan, gd, in, sp);
   return SPD_OK;
 }
 
@@ -975,7 +1102,8 @@ int spd_step_range(const spd_plan* plan, const spd_grid_desc* gd, const void* in
   int rc = check_desc(plan, gd);
   if (rc) return rc;
   StepParams sp;
-  fill_step_params(plan, gd, in, out, lo, hi, sp);
+  rc = fill_step_params(plan, gd, in, out, lo, hi, sp);
+  if (rc) return rc;
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
 
@@ -987,7 +1115,8 @@ int spd_run(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* buf
   StepParams sp;
   int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
   for (int s = 0; s < steps; ++s) {
-    fill_step_params(plan, gd, s % 2 ? buf1 : buf0, s % 2 ? buf0 : buf1, 0, extent, sp);
+    rc = fill_step_params(plan, gd, s % 2 ? buf1 : buf0, s % 2 ? buf0 : buf1, 0, extent, sp);
+    if (rc) return rc;
     rc = dispatch(plan, sp, (cudaStream_t)stream);
     if (rc) return rc;
   }
