@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -183,6 +184,7 @@ struct StepParams {
   int tiles_x, tiles_y, tiles_z;
   int tile_y0, tile_z0;      // first tile row / plane of the range
   int n_tiles;
+  int reverse;               // traverse tiles last-to-first (L2 reuse across steps)
   const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
   const uint32_t* e_words;   // [S][128]
 };
@@ -336,6 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   T* __restrict__ out = static_cast<T*>(p.out);
 
   auto tile_origin = [&](int t, int64_t& z0, int64_t& y0, int64_t& x0) {
+    if (p.reverse) t = p.n_tiles - 1 - t;
     int bx = t % p.tiles_x;
     int rest = t / p.tiles_x;
     int by = rest % p.tiles_y;
@@ -810,19 +813,12 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
 template <typename T, int PARITY>
 static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   const Geometry& g = plan->g;
-  // items per producer warp: ceil(r_in * segs / 8)
-  if (g.L == 4 && g.n_tile == 128) {
-    // 2D (r_in 34, 2 segs -> 68 items) and 1D (r_in 32 -> 64 items)
-    return launch_step<T, 4, PARITY, 128, 1, 4, 3, 9>(plan, sp, st);
-  }
-  if (g.L == 4 && g.n_tile == 64) {
-    // 3D: r_in 60, 1 seg -> 60 items
-    return launch_step<T, 4, PARITY, 64, 1, 5, 4, 8>(plan, sp, st);
-  }
-  if (g.L == 8 && g.n_tile == 64) {
-    // 2D r=3: r_in 22, 2 segs -> 44 items; 1D: 16 rows -> 32 items
-    return launch_step<T, 8, PARITY, 64, 2, 5, 4, 6>(plan, sp, st);
-  }
+  // <T, L, PARITY, NTILE, B-image stages, natural-row stages, accumulator
+  //  stages, items per producer warp>; stage counts fill the 227 KB of smem
+  // (scan in profiles/r01_tuning.txt).
+  if (g.L == 4 && g.n_tile == 128) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 9>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 64) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 8>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 6>(plan, sp, st);
   return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
 }
 
@@ -1117,6 +1113,9 @@ int spd_run(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* buf
   for (int s = 0; s < steps; ++s) {
     rc = fill_step_params(plan, gd, s % 2 ? buf1 : buf0, s % 2 ? buf0 : buf1, 0, extent, sp);
     if (rc) return rc;
+    // Alternate the traversal direction: step s+1 starts on the tiles step s
+    // wrote last, which are still resident in the 126 MB L2.
+    sp.reverse = s & 1;
     rc = dispatch(plan, sp, (cudaStream_t)stream);
     if (rc) return rc;
   }
