@@ -185,11 +185,13 @@ struct StepParams {
   int tile_y0, tile_z0;      // first tile row / plane of the range
   int n_tiles;
   int reverse;               // traverse tiles last-to-first (L2 reuse across steps)
+  int dbg;                   // development switches (SPD_DBG), 0 in production
+  int prefetch;              // L2 prefetch distance in tiles (0 = off)
   const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
   const uint32_t* e_words;   // [S][128]
 };
 
-constexpr int kEpiWarps = 4;
+constexpr int kEpiWarps = 4;   // one warp per TMEM lane quadrant
 constexpr int kProdWarps = 8;
 constexpr int kMmaWarp = kEpiWarps + kProdWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;
@@ -241,11 +243,30 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+// Tensor box prefetch into L2 (no smem, no completion): lets the loader run
+// further ahead than the natural-row ring allows.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
 __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
+// Predicated 32-bit shared load: v keeps its value where pred is false (no
+// divergent branch around it).
+__device__ __forceinline__ void lds_u32_if(uint32_t& v, bool pred, uint32_t addr) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %1, 0;\n@p ld.shared.u32 %0, [%2];\n}" : "+r"(v) : "r"((uint32_t)pred), "r"(addr));
+}
+
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -259,7 +280,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 //   loader --(nat_full: tx bytes)--> producers --(nat_empty)--> loader
 //   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
 //   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ, int RIN>
 __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
   using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, NQ>;
   constexpr int KC = C::KC;
@@ -360,20 +381,35 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         const uint32_t nphase = (it / NNAT) & 1;
         int64_t z0, y0, x0;
         tile_origin(t, z0, y0, x0);
-        mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
         const uint32_t dst = nat_s + ns * p.nat_bytes;
         const uint32_t fb = bar_natf + 8 * ns;
         if (p.use_tmap) {
+          auto issue = [&](int tt, bool prefetch) {
+            int64_t pz, py, px;
+            tile_origin(tt, pz, py, px);
+            const int c0 = (int)(p.xoff + px - 8);
+            const int c1 = (int)(p.yoff + py - g.r);
+            const int c2 = (int)(p.zoff + pz - g.r);
+            for (int k = 0; k < p.nbox; ++k) {
+              if (g.d == 3) {
+                if (prefetch) tma_prefetch_3d(&p.tmap, c0 + k * p.boxw, c1, c2);
+                else tma_load_3d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, c2, fb);
+              } else {
+                if (prefetch) tma_prefetch_2d(&p.tmap, c0 + k * p.boxw, c1);
+                else tma_load_2d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, fb);
+              }
+            }
+          };
+          if (it == 0)  // warm the first prefetch window
+            for (int j = 1; j < p.prefetch; ++j)
+              if (t + j * (int)gridDim.x < p.n_tiles) issue(t + j * (int)gridDim.x, true);
+          if (p.prefetch > 0 && t + p.prefetch * (int)gridDim.x < p.n_tiles)
+            issue(t + p.prefetch * (int)gridDim.x, true);
+          mbar_wait(bar_nate + 8 * ns, nphase ^ 1);  // prefetches go out before the ring wait
           mbar_arrive_expect_tx(fb, box_bytes * p.nbox);
-          const int c0 = (int)(p.xoff + x0 - 8);
-          const int c1 = (int)(p.yoff + y0 - g.r);
-          if (g.d == 3) {
-            const int c2 = (int)(p.zoff + z0 - g.r);
-            for (int k = 0; k < p.nbox; ++k) tma_load_3d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, c2, fb);
-          } else {
-            for (int k = 0; k < p.nbox; ++k) tma_load_2d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, fb);
-          }
+          issue(t, false);
         } else {
+          mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
           mbar_arrive_expect_tx(fb, (uint32_t)(g.r_in * C::ROW_BYTES));
           const T* tbase = in + p.origin + z0 * p.plane + y0 * p.pitch + x0 - 8;
           for (int b = 0; b < g.r_in; ++b) {
@@ -386,15 +422,24 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   } else if (warp >= kEpiWarps && warp < kMmaWarp) {
     // ===================== producer: natural rows -> permuted B image =====
     const int pw = warp - kEpiWarps;
-    const int n_items = g.r_in * C::SEGS;
+    constexpr int n_items = RIN * C::SEGS;
+    static_assert((NQ - 1) * kProdWarps < n_items && NQ * kProdWarps >= n_items, "NQ must cover the items");
     constexpr int R = (L - 2) / 2;
     // ext[] words actually referenced by the windows (compile time):
     //   element e of ext is x = 8*lane - 8 + e; windows span
     //   e in [8 - R, 8 + (CPL-1)*L - R + 2L - 1]
     constexpr int kPrevW = (8 - R) / 2;                                     // first prev word used
     constexpr int kNextW = (8 + (C::CPL - 1) * L - R + 2 * L - 1) / 2 - 8;  // last next word used
-    // Loop-invariant per-item offsets: natural-stage byte offset of the lane's
-    // 16 B and the lane's B-image byte offset.
+    // Loop-invariant per-item offsets: natural-stage byte offsets of the lane's
+    // 16 B and of its neighbouring groups (edges, lanes 0/31 only), and the
+    // B-image byte offset of the lane's first chunk.
+    //
+    // B-image column order (CPL = 2): chunk n sits at column
+    //   sigma(n) = (n & ~15) | ((n & 1) << 3) | ((n >> 1) & 7),
+    // i.e. even chunks fill one 8-row core-matrix group and odd chunks the
+    // next.  Each STS.128 (all lanes storing their even, then their odd chunk)
+    // then covers the 32 banks once per quarter-warp — conflict-free without
+    // per-lane selects.  The epilogue undoes sigma when it pairs D columns.
     uint32_t noff[NQ], poff[NQ], xoff_n[NQ], soff[NQ];
     bool valid[NQ];
     // natural stage: element x of row b at box k = x / boxw
@@ -405,19 +450,19 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
       const int item = pw + q * kProdWarps;
-      valid[q] = item < n_items;
+      valid[q] = q < NQ - 1 || item < n_items;  // only the last slot can be empty
       const int b = valid[q] ? item / C::SEGS : 0, sg = valid[q] ? item % C::SEGS : 0;
       const int xl = 8 + sg * 256 + lane * 8;  // this lane's 8 points (stage-local x)
       noff[q] = nat_addr(b, xl);
-      poff[q] = nat_addr(b, xl - 8);
+      poff[q] = nat_addr(b, xl - 8) + 4 * kPrevW;
       xoff_n[q] = nat_addr(b, xl + 8);
       const int n0 = sg * C::SEG + lane * C::CPL;
-      soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(n0 / 8) * sbo + (n0 % 8) * 16;
+      const int col = C::CPL == 2 ? ((n0 & ~15) | ((n0 >> 1) & 7)) : n0;
+      soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(col / 8) * sbo + (col % 8) * 16;
     }
-    // CPL = 2: lanes 4-7 of a quarter-warp hit the next core-matrix group at
-    // the same bank offsets as lanes 0-3; they store their odd chunk first so
-    // every STS.128 phase covers the 32 banks once.
-    const bool flip = C::CPL == 2 && ((lane >> 2) & 1);
+    constexpr int kPW = 4 - kPrevW;  // prev words needed by lane 0
+    constexpr int kNW = kNextW + 1;  // next words needed by lane 31
+    constexpr int kEW = kPW > kNW ? kPW : kNW;
     int it = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
@@ -426,55 +471,58 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       const uint32_t nphase = (it / NNAT) & 1;
       const uint32_t nbase = nat_s + ns * p.nat_bytes;
       mbar_wait(bar_natf + 8 * ns, nphase);
-      mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
-      const uint32_t sbase = bimg_s + stage * stage_bytes;
+      // phase 1: all shared-memory reads of the tile (ILP across items)
+      uint4 cur[NQ];
+      uint32_t edge[NQ][kEW];
+      const bool l0 = lane == 0, l31 = lane == 31;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        if (valid[q]) {
-          const uint4 cur = lds_v4(nbase + noff[q]);
+        if (valid[q] && !(p.dbg & 4)) {
+          cur[q] = lds_v4(nbase + noff[q]);
+#pragma unroll
+          for (int w = 0; w < kEW; ++w) {
+            edge[q][w] = 0;
+            if (w < kPW) lds_u32_if(edge[q][w], l0, nbase + poff[q] + 4 * w);
+            if (w < kNW) lds_u32_if(edge[q][w], l31, nbase + xoff_n[q] + 4 * w);
+          }
+        }
+      }
+      mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+      const uint32_t sbase = bimg_s + stage * stage_bytes;
+      // phase 2: neighbour exchange, permutation, B-image stores
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (valid[q] && !(p.dbg & 4)) {
           uint32_t ext[12];
-          const uint32_t cw[4] = {cur.x, cur.y, cur.z, cur.w};
+          const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) ext[4 + w] = cw[w];
 #pragma unroll
           for (int w = kPrevW; w < 4; ++w) {
-            ext[w] = __shfl_up_sync(0xffffffffu, cw[w], 1);
-            if (lane == 0) ext[w] = lds_u32(nbase + poff[q] + 4 * w);
+            const uint32_t v = __shfl_up_sync(0xffffffffu, cw[w], 1);
+            ext[w] = l0 ? edge[q][w - kPrevW] : v;
           }
 #pragma unroll
           for (int w = 0; w <= kNextW; ++w) {
-            ext[8 + w] = __shfl_down_sync(0xffffffffu, cw[w], 1);
-            if (lane == 31) ext[8 + w] = lds_u32(nbase + xoff_n[q] + 4 * w);
+            const uint32_t v = __shfl_down_sync(0xffffffffu, cw[w], 1);
+            ext[8 + w] = l31 ? edge[q][w] : v;
           }
-          uint32_t wd[C::CPL][KC][4];
+          const uint32_t a0 = sbase + soff[q];
 #pragma unroll
-          for (int c = 0; c < C::CPL; ++c)
+          for (int c = 0; c < C::CPL; ++c) {
+            // CPL = 2: the odd chunk lives in the next core-matrix group
+            const uint32_t ac = a0 + (c ? (uint32_t)sbo : 0u);
 #pragma unroll
-            for (int kc = 0; kc < KC; ++kc)
+            for (int kc = 0; kc < KC; ++kc) {
+              uint32_t wd[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
                 const int e0 = 8 + c * L - R + perm_slot(L, PARITY, 8 * kc + 2 * u);
                 const int e1 = 8 + c * L - R + perm_slot(L, PARITY, 8 * kc + 2 * u + 1);
-                wd[c][kc][u] = __byte_perm(ext[e0 / 2], ext[e1 / 2], sel_halves(e0 % 2, e1 % 2));
+                wd[u] = __byte_perm(ext[e0 / 2], ext[e1 / 2], sel_halves(e0 % 2, e1 % 2));
               }
-          const uint32_t a0 = sbase + soff[q];
-          if (C::CPL == 2) {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const int ci = c ^ (int)flip;
-              const uint32_t addr = a0 + (ci ? 16u : 0u);  // chunks n0, n0+1: adjacent core-matrix rows
-#pragma unroll
-              for (int kc = 0; kc < KC; ++kc) {
-                const uint32_t v0 = ci ? wd[C::CPL - 1][kc][0] : wd[0][kc][0];
-                const uint32_t v1 = ci ? wd[C::CPL - 1][kc][1] : wd[0][kc][1];
-                const uint32_t v2 = ci ? wd[C::CPL - 1][kc][2] : wd[0][kc][2];
-                const uint32_t v3 = ci ? wd[C::CPL - 1][kc][3] : wd[0][kc][3];
-                sts_v4(addr + kc * 128, v0, v1, v2, v3);
-              }
+              sts_v4(ac + kc * 128, wd[0], wd[1], wd[2], wd[3]);
             }
-          } else {
-#pragma unroll
-            for (int kc = 0; kc < KC; ++kc) sts_v4(a0 + kc * 128, wd[0][kc][0], wd[0][kc][1], wd[0][kc][2], wd[0][kc][3]);
           }
         }
       }
@@ -502,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
 #pragma unroll
         for (int s = 0; s < SPD_MAX_S; ++s) {
-          if (s < g.s) {
+          if (s < g.s && !(p.dbg & 8)) {
             const uint64_t bdesc = umma_desc(sbase + g.start_row[s] * KC * 128, 128, sbo);
             mma_sp_ts(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
           }
@@ -514,10 +562,11 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
   } else {
     // ===================== epilogue ========================================
-    const int m = warp * 32 + lane;  // TMEM lane == M row
+    const int quad = warp;  // TMEM lane quadrant
+    const int m = quad * 32 + lane;  // TMEM lane == M row
     const int alpha = m / L;         // output row of the tile
     const int d = lane % L;          // position in the L-lane group
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
     int it = 0;
     for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
@@ -546,14 +595,22 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
         }
-        // pack pairs of columns: pk[j] = (col 2j, col 2j+1) of my lane
+        if (p.dbg & 2) continue;
+        // pack chunk pairs: pk[j] = (chunk 2j, chunk 2j+1) of this batch; with
+        // the sigma column order (CPL = 2) chunk 2j sits at column
+        // (j/8)*16 + j%8 and chunk 2j+1 eight columns later.
         uint32_t pk[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = Cvt<T>::pack(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]));
+        for (int j = 0; j < 16; ++j) {
+          const int c0 = C::CPL == 2 ? (j / 8) * 16 + (j % 8) : 2 * j;
+          const int c1 = C::CPL == 2 ? c0 + 8 : 2 * j + 1;
+          pk[j] = Cvt<T>::pack(__uint_as_float(v[c0]), __uint_as_float(v[c1]));
+        }
         // xor-butterfly transpose inside the L-lane group: pk[k*L + dd] goes
         // to lane dd; afterwards pk[k*L + s] holds source lane s's word.
 #pragma unroll
         for (int b = 1; b < L; b <<= 1) {
+          if (p.dbg & 16) break;
           const bool upper = (d & b) != 0;
 #pragma unroll
           for (int k = 0; k < 16 / L; ++k) {
@@ -567,7 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             }
           }
         }
-        if (row_ok) {
+        if (row_ok && !(p.dbg & 1)) {
 #pragma unroll
           for (int k = 0; k < 16 / L; ++k) {
             // this lane now owns 2L consecutive points starting at chunk c0
@@ -782,10 +839,11 @@ struct spd_plan {
 
 namespace spd {
 
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ, int RIN>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
   using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, NQ>;
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, NQ>;
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, NQ, RIN>;
+  if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
   sp.nat_bytes = sp.use_tmap ? sp.nbox * sp.box_slot : plan->g.r_in * C::ROW_BYTES;
   if (!sp.use_tmap) {
     sp.nbox = 1;
@@ -816,9 +874,11 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   // <T, L, PARITY, NTILE, B-image stages, natural-row stages, accumulator
   //  stages, items per producer warp>; stage counts fill the 227 KB of smem
   // (scan in profiles/r01_tuning.txt).
-  if (g.L == 4 && g.n_tile == 128) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 9>(plan, sp, st);
-  if (g.L == 4 && g.n_tile == 64) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 8>(plan, sp, st);
-  if (g.L == 8 && g.n_tile == 64) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 6>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 128 && g.r_in == 34) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 9, 34>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 8, 32>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 64 && g.r_in == 60) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 8, 60>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 6, 22>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 4, 16>(plan, sp, st);
   return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
 }
 
@@ -913,6 +973,10 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     sp.tiles_y = sp.tiles_z = 1;
   }
   sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
+  static const char* dbg_env = getenv("SPD_DBG");
+  sp.dbg = dbg_env ? atoi(dbg_env) : 0;
+  static const char* pf_env = getenv("SPD_PREFETCH");
+  sp.prefetch = pf_env ? atoi(pf_env) : 2;
   sp.zoff = (int)(gd->origin / gd->plane);
   sp.yoff = (int)((gd->origin % gd->plane) / gd->pitch);
   sp.xoff = (int)(gd->origin % gd->pitch);
