@@ -35,6 +35,17 @@ namespace spd {
 // ---------------------------------------------------------------------------
 // PTX helpers
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
+  return t;
+}
+// Debug timeline: event e of tile-iteration it in CTA 0 (64 iterations max).
+#define SPD_TRACE(e, it)                                                            \
+  do {                                                                              \
+    if (p.trace && blockIdx.x == 0 && (it) < 64) p.trace[(e) * 64 + (it)] = gtimer(); \
+  } while (0)
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -119,6 +130,14 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&v)[32]) {
       : "r"(taddr));
 }
 
+// 256-bit global store (sm_100): one full 32-B sector group per lane.
+__device__ __forceinline__ void stg_v8(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e, uint32_t f,
+                                       uint32_t g, uint32_t h) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d), "r"(e),
+               "r"(f), "r"(g), "r"(h)
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -187,6 +206,7 @@ struct StepParams {
   int reverse;               // traverse tiles last-to-first (L2 reuse across steps)
   int dbg;                   // development switches (SPD_DBG), 0 in production
   int prefetch;              // L2 prefetch distance in tiles (0 = off)
+  unsigned long long* trace; // debug timeline (CTA 0): [event][tile] globaltimer stamps, or null
   const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
   const uint32_t* e_words;   // [S][128]
 };
@@ -303,6 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) SPD_TRACE(13, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -357,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 
   const T* __restrict__ in = static_cast<const T*>(p.in);
   T* __restrict__ out = static_cast<T*>(p.out);
+  if (threadIdx.x == 0) SPD_TRACE(14, 0);
 
   auto tile_origin = [&](int t, int64_t& z0, int64_t& y0, int64_t& x0) {
     if (p.reverse) t = p.n_tiles - 1 - t;
@@ -405,9 +427,11 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
               if (t + j * (int)gridDim.x < p.n_tiles) issue(t + j * (int)gridDim.x, true);
           if (p.prefetch > 0 && t + p.prefetch * (int)gridDim.x < p.n_tiles)
             issue(t + p.prefetch * (int)gridDim.x, true);
+          SPD_TRACE(0, it);
           mbar_wait(bar_nate + 8 * ns, nphase ^ 1);  // prefetches go out before the ring wait
           mbar_arrive_expect_tx(fb, box_bytes * p.nbox);
           issue(t, false);
+          SPD_TRACE(1, it);
         } else {
           mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
           mbar_arrive_expect_tx(fb, (uint32_t)(g.r_in * C::ROW_BYTES));
@@ -471,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       const uint32_t nphase = (it / NNAT) & 1;
       const uint32_t nbase = nat_s + ns * p.nat_bytes;
       mbar_wait(bar_natf + 8 * ns, nphase);
+      if (pw == 0 && lane == 0) SPD_TRACE(2, it);
       // phase 1: all shared-memory reads of the tile (ILP across items)
       uint4 cur[NQ];
       uint32_t edge[NQ][kEW];
@@ -488,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         }
       }
       mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+      if (pw == 0 && lane == 0) SPD_TRACE(3, it);
       const uint32_t sbase = bimg_s + stage * stage_bytes;
       // phase 2: neighbour exchange, permutation, B-image stores
 #pragma unroll
@@ -531,6 +557,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       if (lane == 0) {
         mbar_arrive(bar_nate + 8 * ns);
         mbar_arrive(bar_full + 8 * stage);
+        if (pw == 0) SPD_TRACE(4, it);
+        if (pw == kProdWarps - 1) SPD_TRACE(5, it);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -543,9 +571,11 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       const int acc = it % NACC;
       const uint32_t aphase = (it / NACC) & 1;
       mbar_wait(bar_acce + 8 * acc, aphase ^ 1);
+      if (lane == 0) SPD_TRACE(6, it);
       mbar_wait(bar_full + 8 * stage, sphase);
       tc_fence_after();
       if (lane == 0) {
+        SPD_TRACE(7, it);
         const uint32_t sbase = bimg_s + stage * stage_bytes;
         const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
 #pragma unroll
@@ -585,74 +615,96 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       T* orow = out + p.origin + z * p.plane + y * p.pitch + xr;
       mbar_wait(bar_accf + 8 * acc, aphase);
       tc_fence_after();
-#pragma unroll 1
-      for (int cb = 0; cb < NTILE / 32; ++cb) {
-        uint32_t v[32];
-        tmem_ld_x32(lane_base + C::ACC_COL + acc * NTILE + cb * 32, v);
-        tmem_wait_ld();
-        if (cb == NTILE / 32 - 1) {
+      if (warp == 0 && lane == 0) SPD_TRACE(8, it);
+      // Per 32-column batch: pack chunk pairs to 16-bit, xor-butterfly inside
+      // the L-lane group so each lane ends up owning 2*PPD consecutive chunks
+      // (32 points = 64 B), then two 256-bit full-line stores.  TMEM loads are
+      // double-buffered: batch cb+1 is in flight while cb is transposed.
+      constexpr int NB = NTILE / 32;
+      constexpr int PPD = 16 / L;  // packed words (chunk pairs) per destination lane
+      const uint32_t tcol = lane_base + C::ACC_COL + acc * NTILE;
+      uint32_t va[32], vb[32];
+      tmem_ld_x32(tcol, va);
+      tmem_wait_ld();
+#pragma unroll
+      for (int cb = 0; cb < NB; ++cb) {
+        uint32_t(&v)[32] = (cb & 1) ? vb : va;
+        uint32_t(&vn)[32] = (cb & 1) ? va : vb;
+        if (cb + 1 < NB) tmem_ld_x32(tcol + (cb + 1) * 32, vn);
+        if (cb == NB - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
         }
-        if (p.dbg & 2) continue;
-        // pack chunk pairs: pk[j] = (chunk 2j, chunk 2j+1) of this batch; with
-        // the sigma column order (CPL = 2) chunk 2j sits at column
-        // (j/8)*16 + j%8 and chunk 2j+1 eight columns later.
-        uint32_t pk[16];
+        if (warp == 0 && lane == 0 && cb == 0) SPD_TRACE(10, it);
+        // bw[k*L + dd] = chunk pair (2j, 2j+1), j = dd*PPD + k, destined to
+        // lane dd of the group.  With the sigma column order (CPL = 2) chunk
+        // 2j sits at column (j/8)*16 + j%8 and chunk 2j+1 eight columns later.
+        uint32_t bw[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int c0 = C::CPL == 2 ? (j / 8) * 16 + (j % 8) : 2 * j;
-          const int c1 = C::CPL == 2 ? c0 + 8 : 2 * j + 1;
-          pk[j] = Cvt<T>::pack(__uint_as_float(v[c0]), __uint_as_float(v[c1]));
-        }
-        // xor-butterfly transpose inside the L-lane group: pk[k*L + dd] goes
-        // to lane dd; afterwards pk[k*L + s] holds source lane s's word.
+        for (int dd = 0; dd < L; ++dd)
+#pragma unroll
+          for (int k = 0; k < PPD; ++k) {
+            const int j = dd * PPD + k;
+            const int c0 = C::CPL == 2 ? (j / 8) * 16 + (j % 8) : 2 * j;
+            const int c1 = C::CPL == 2 ? c0 + 8 : 2 * j + 1;
+            bw[k * L + dd] = Cvt<T>::pack(__uint_as_float(v[c0]), __uint_as_float(v[c1]));
+          }
 #pragma unroll
         for (int b = 1; b < L; b <<= 1) {
           if (p.dbg & 16) break;
           const bool upper = (d & b) != 0;
 #pragma unroll
-          for (int k = 0; k < 16 / L; ++k) {
+          for (int k = 0; k < PPD; ++k) {
 #pragma unroll
             for (int dd = 0; dd < L; ++dd) {
               if (dd & b) continue;
-              uint32_t send = upper ? pk[k * L + dd] : pk[k * L + (dd | b)];
-              uint32_t recv = __shfl_xor_sync(0xffffffffu, send, b);
-              if (upper) pk[k * L + dd] = recv;
-              else pk[k * L + (dd | b)] = recv;
+              const uint32_t send = upper ? bw[k * L + dd] : bw[k * L + (dd | b)];
+              const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, b);
+              if (upper) bw[k * L + dd] = recv;
+              else bw[k * L + (dd | b)] = recv;
             }
           }
         }
+        if (warp == 0 && lane == 0 && cb == 0) SPD_TRACE(11, it);
+        // lane d now holds bw[k*L + s] = source lane s's pair (chunks 2(d*PPD+k),
+        // +1): 2*PPD consecutive chunks from c_lane; build the 16 output words
+        // (x = L*chunk + s, pairs of s) in ascending x.
         if (row_ok && !(p.dbg & 1)) {
+          uint32_t w[16];
 #pragma unroll
-          for (int k = 0; k < 16 / L; ++k) {
-            // this lane now owns 2L consecutive points starting at chunk c0
-            const int64_t c0 = (int64_t)cb * 32 + 2 * L * k + 2 * d;
-            uint32_t w[L];
+          for (int k = 0; k < PPD; ++k)
 #pragma unroll
-            for (int tt = 0; tt < L; ++tt) {
-              const int e = 2 * tt;
-              if (e < L) w[tt] = __byte_perm(pk[k * L + e], pk[k * L + e + 1], 0x5410);
-              else w[tt] = __byte_perm(pk[k * L + e - L], pk[k * L + e - L + 1], 0x7632);
-            }
-            T* dst = orow + c0 * L;
-            if (c0 + 1 < chunk_lim) {
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-              for (int q = 0; q < L / 4; ++q)
-                *reinterpret_cast<uint4*>(dst + 8 * q) = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-            } else if (c0 < chunk_lim) {
-              if (L == 4) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-              else *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+              for (int u = 0; u < L / 2; ++u)
+                w[(2 * k + h) * (L / 2) + u] =
+                    __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
+          const int64_t c_lane = (int64_t)cb * 32 + 2 * PPD * d;
+          T* dst = orow + c_lane * L;
+          if (c_lane + 2 * PPD <= chunk_lim) {
+            stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+            stg_v8(dst + 16, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2 * PPD; ++c) {
+              if (c_lane + c < chunk_lim) {
+                if (L == 4) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(w[2 * c], w[2 * c + 1]);
+                else *reinterpret_cast<uint4*>(dst + c * L) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+              }
             }
           }
         }
+        if (warp == 0 && lane == 0 && cb == 0) SPD_TRACE(12, it);
+        if (cb + 1 < NB) tmem_wait_ld();
       }
+      if (warp == 0 && lane == 0) SPD_TRACE(9, it);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) SPD_TRACE(15, 0);
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
@@ -891,6 +943,8 @@ static int dispatch(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
 
 static int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+static unsigned long long* g_trace = nullptr;  // debug timeline buffer (SPD_TRACE)
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -976,7 +1030,12 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
   static const char* dbg_env = getenv("SPD_DBG");
   sp.dbg = dbg_env ? atoi(dbg_env) : 0;
   static const char* pf_env = getenv("SPD_PREFETCH");
-  sp.prefetch = pf_env ? atoi(pf_env) : 2;
+  sp.prefetch = pf_env ? atoi(pf_env) : 0;
+  sp.trace = nullptr;
+  if (getenv("SPD_TRACE")) {
+    if (!g_trace) cudaMalloc(&g_trace, 16 * 64 * sizeof(unsigned long long));
+    sp.trace = g_trace;
+  }
   sp.zoff = (int)(gd->origin / gd->plane);
   sp.yoff = (int)((gd->origin % gd->plane) / gd->pitch);
   sp.xoff = (int)(gd->origin % gd->pitch);
@@ -1121,7 +1180,9 @@ int spd_grid_layout(const spd_plan* plan, int64_t nz, int64_t ny, int64_t nx, in
   const Geometry& g = plan->g;
   if (plan->d == 2 && nz != 1) return set_error(SPD_EINVAL, "2D grid must have nz = 1");
   if (plan->d == 1 && (nz != 1 || ny != 1)) return set_error(SPD_EINVAL, "1D grid must have nz = ny = 1");
-  const int64_t xoff = roundup(halo > 8 ? halo : 8, 8);
+  // x = 0 sits 32-B aligned (256-bit epilogue stores); >= 8 elements of left
+  // margin for the 16-B groups left of the first chunk window
+  const int64_t xoff = roundup(halo > 8 ? halo : 8, 16);
   const int64_t nx_pad = roundup(nx, g.tile_x);
   int64_t need_x = nx_pad + 8 > nx + halo ? nx_pad + 8 : nx + halo;
   const int64_t pitch = roundup(xoff + need_x, 64);
@@ -1286,6 +1347,12 @@ int spd_naive_apply_f64(int d, int r, const double* coeffs, int64_t nz, int64_t 
   }
   cudaFreeAsync(w, st);
   return cuda_err(cudaGetLastError(), "naive_f64_kernel");
+}
+
+// Debug: copy the CTA-0 timeline of the last traced launch (16 x 64 stamps).
+extern "C" int spd_debug_trace(unsigned long long* host) {
+  if (!spd::g_trace) return spd::set_error(SPD_EINVAL, "no trace (set SPD_TRACE and run a step)");
+  return spd::cuda_err(cudaMemcpy(host, spd::g_trace, 16 * 64 * 8, cudaMemcpyDeviceToHost), "trace copy");
 }
 
 int spd_mma_selftest(const uint16_t* a, const uint8_t* e, const uint16_t* b, int n, float* d, void* stream) {
