@@ -258,7 +258,7 @@ def run_ours(args, cfg_name):
 
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     dense_shape = tuple(s + 2 * r for s in shape)
-    if world == 1:
+    if world == 1 and not args.force_slab:
         grid = DeviceGrid(plan, shape, r)
         dense = torch.rand(dense_shape, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
         grid.load_dense_f64(dense)
@@ -322,8 +322,9 @@ def run_ours(args, cfg_name):
     # point per timestep (fp16 read + write), SURVEY.md §8(d)
     hbm, peak_kind = measured_peaks()
     n_launch = args.steps * T
-    launch_s = (ms / 1e3) / n_launch if world == 1 else None
-    if world == 1:
+    slab_mode = world > 1 or args.force_slab
+    launch_s = (ms / 1e3) / n_launch if not slab_mode else None
+    if not slab_mode:
         achieved = 4.0 * points_local / launch_s / 1e9
     else:
         achieved = 4.0 * points_local * T * args.steps / (ms / 1e3) / 1e9
@@ -336,7 +337,7 @@ def run_ours(args, cfg_name):
 
     # end to end through the public API: pinned host fp16 grid in, result out
     e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if rank == 0 and world == 1 and not args.no_e2e and not args.force_slab:
         host_in = torch.empty(dense_shape, dtype=torch.float16, pin_memory=True)
         host_in.copy_((torch.rand(dense_shape, dtype=torch.float32) * 2 - 1).half())
         host_out = torch.empty_like(host_in, pin_memory=True)
@@ -380,14 +381,14 @@ def run_ours(args, cfg_name):
             "dtype": "fp16",
             "data": "synthetic U(-1,1) grid, contractive normalised weights (random init)",
             "config": {"workload": cfg_name, "description": desc, "grid_per_gpu": list(shape),
-                       "timesteps_per_step": T, "parallelism": f"slab{world}" if world > 1 else "single",
+                       "timesteps_per_step": T, "parallelism": f"slab{world}" if slab_mode else "single",
                        "l2": f"inputs larger than L2 ({2 * np.prod(dense_shape) / 2**20:.0f} MiB per buffer)",
                        "tile": {"L": info.L, "n_tile": info.n_tile, "mmas_per_tile": info.mmas_per_tile},
                        "slab": slab},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": n_launch if world == 1 else args.steps * launches_per_step,
+            "gpu_launches": n_launch if not slab_mode else args.steps * launches_per_step,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -405,6 +406,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--force-slab", action="store_true", help="use the multi-GPU slab driver even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

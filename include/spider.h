@@ -144,6 +144,13 @@ int spd_grid_layout(const spd_plan* plan, int64_t nz, int64_t ny, int64_t nx,
 int spd_run(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
             void* buf1, int steps, void* stream);
 
+/* spd_run with flags: SPD_RUN_PERSISTENT runs all steps in one cooperative
+ * launch ordered by per-band completion counters instead of one launch per
+ * step (same results bit for bit). */
+#define SPD_RUN_PERSISTENT 1
+int spd_run_ex(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
+               void* buf1, int steps, int flags, void* stream);
+
 /* One step restricted to output rows [y_begin, y_end) (2D) or planes
  * [z_begin, z_end) (3D) — used by the slab driver to compute the boundary
  * bands before the halo exchange and the interior after. */

@@ -72,6 +72,7 @@ SIGNATURES = {
     "spd_plan_geometry": (_I, [_P, _I32, _I32]),
     "spd_grid_layout": (_I, [_P, _I64, _I64, _I64, _I, _DESC]),
     "spd_run": (_I, [_P, _DESC, _P, _P, _I, _P]),
+    "spd_run_ex": (_I, [_P, _DESC, _P, _P, _I, _I, _P]),
     "spd_step_range": (_I, [_P, _DESC, _P, _P, _I64, _I64, _P]),
     "spd_pack_grid": (_I, [_DESC, _I, _P, _P, _P]),
     "spd_unpack_grid": (_I, [_DESC, _I, _P, _P, _P]),

@@ -41,9 +41,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 // Debug timeline: event e of tile-iteration it in CTA 0 (64 iterations max).
-#define SPD_TRACE(e, it)                                                            \
-  do {                                                                              \
-    if (p.trace && blockIdx.x == 0 && (it) < 64) p.trace[(e) * 64 + (it)] = gtimer(); \
+#define SPD_TRACE(e, it)                                                                                 \
+  do {                                                                                                   \
+    if (p.trace && blockIdx.x < 8 && (it) < 64) *(volatile unsigned long long*)&p.trace[(blockIdx.x * 16 + (e)) * 64 + (it)] = gtimer(); \
   } while (0)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -188,14 +188,16 @@ __host__ __device__ constexpr uint32_t sel_halves(int ha, int hb) {
 // Kernel parameters
 
 struct StepParams {
-  CUtensorMap tmap;          // input grid as a 2D / 3D tensor (tensor-TMA mode)
+  CUtensorMap tmap[2];       // buf[0] / buf[1] as 2D / 3D tensors (tensor-TMA mode)
   Geometry g;
   int use_tmap;              // 1: tensor-TMA boxes, 0: 1D bulk copies per row
   int nbox, boxw, box_slot;  // natural-stage layout: [box][row][boxw] elements
   int nat_bytes;             // bytes per natural stage
   int xoff, yoff, zoff;      // stored coordinates of interior (0, 0, 0)
-  const void* in;
-  void* out;
+  void* buf[2];              // step t reads buf[t & 1] and writes buf[(t + 1) & 1]
+  int steps;                 // Jacobi steps in this launch (persistent, >= 1)
+  unsigned int* band_done;   // [n_bands] completed tiles per band (steps > 1)
+  int per_band, n_bands;     // tiles per band; bands (2D: tile rows, 3D: tile planes, 1D: tiles)
   int64_t pitch, plane, origin;
   int64_t nx;                // x extent (interior)
   int64_t row_lo, row_hi;    // valid output rows (2D: y, 3D: z, 1D: unused)
@@ -203,7 +205,7 @@ struct StepParams {
   int tiles_x, tiles_y, tiles_z;
   int tile_y0, tile_z0;      // first tile row / plane of the range
   int n_tiles;
-  int reverse;               // traverse tiles last-to-first (L2 reuse across steps)
+  int reverse;               // step 0 traverses tiles last-to-first; steps alternate
   int dbg;                   // development switches (SPD_DBG), 0 in production
   int prefetch;              // L2 prefetch distance in tiles (0 = off)
   unsigned long long* trace; // debug timeline (CTA 0): [event][tile] globaltimer stamps, or null
@@ -274,6 +276,12 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(reinterpret_cast<uint64_t>(map)),
                "r"(c0), "r"(c1), "r"(c2)
                : "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
@@ -376,19 +384,33 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   __syncthreads();
   tc_fence_after();
 
-  const T* __restrict__ in = static_cast<const T*>(p.in);
-  T* __restrict__ out = static_cast<T*>(p.out);
   if (threadIdx.x == 0) SPD_TRACE(14, 0);
-
-  auto tile_origin = [&](int t, int64_t& z0, int64_t& y0, int64_t& x0) {
-    if (p.reverse) t = p.n_tiles - 1 - t;
-    int bx = t % p.tiles_x;
-    int rest = t / p.tiles_x;
-    int by = rest % p.tiles_y;
-    int bz = rest / p.tiles_y;
-    x0 = (int64_t)bx * g.tile_x;
-    y0 = (int64_t)(p.tile_y0 + by) * g.tile_y;
-    z0 = (int64_t)(p.tile_z0 + bz) * g.tile_z;
+  // Work index g in [0, steps * n_tiles): step t = g / n_tiles, tile in the
+  // step's traversal order (alternating direction: each step starts on the
+  // tiles the previous one wrote last, still resident in L2).  Static
+  // round-robin over CTAs; a tile of step t > 0 first waits (loader) for the
+  // three neighbouring bands of step t-1 — dependencies always point to
+  // smaller g, so with all CTAs co-resident (cooperative launch) the smallest
+  // unfinished tile can always proceed.
+  const int total = p.steps * p.n_tiles;
+  struct TileId {
+    int step, band;
+    int64_t z0, y0, x0;
+  };
+  auto decode = [&](int gi) {
+    TileId id;
+    id.step = gi / p.n_tiles;
+    int t = gi - id.step * p.n_tiles;
+    if ((id.step + p.reverse) & 1) t = p.n_tiles - 1 - t;
+    const int bx = t % p.tiles_x;
+    const int rest = t / p.tiles_x;
+    const int by = rest % p.tiles_y;
+    const int bz = rest / p.tiles_y;
+    id.x0 = (int64_t)bx * g.tile_x;
+    id.y0 = (int64_t)(p.tile_y0 + by) * g.tile_y;
+    id.z0 = (int64_t)(p.tile_z0 + bz) * g.tile_z;
+    id.band = g.d == 3 ? bz : (g.d == 2 ? by : bx);
+    return id;
   };
 
   if (warp == kLoadWarp) {
@@ -398,49 +420,47 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     if (lane == 0) {
       const uint32_t box_bytes = (uint32_t)(p.boxw * 2 * g.r_in);
       int it = 0;
-      for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
         const int ns = it % NNAT;
         const uint32_t nphase = (it / NNAT) & 1;
-        int64_t z0, y0, x0;
-        tile_origin(t, z0, y0, x0);
+        const TileId id = decode(gi);
         const uint32_t dst = nat_s + ns * p.nat_bytes;
         const uint32_t fb = bar_natf + 8 * ns;
+        SPD_TRACE(0, it);
+        mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
+        if (id.step > 0) {
+          // RAW/WAR across steps: the previous step's neighbouring bands are
+          // complete (their epilogue stores are visible).
+          const unsigned int need = (unsigned int)(id.step * p.per_band);
+          const int b0 = id.band > 0 ? id.band - 1 : 0;
+          const int b1 = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
+          for (int b = b0; b <= b1; ++b)
+            while (ld_acquire_gpu(p.band_done + b) < need) __nanosleep(64);
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+        }
         if (p.use_tmap) {
-          auto issue = [&](int tt, bool prefetch) {
-            int64_t pz, py, px;
-            tile_origin(tt, pz, py, px);
-            const int c0 = (int)(p.xoff + px - 8);
-            const int c1 = (int)(p.yoff + py - g.r);
-            const int c2 = (int)(p.zoff + pz - g.r);
-            for (int k = 0; k < p.nbox; ++k) {
-              if (g.d == 3) {
-                if (prefetch) tma_prefetch_3d(&p.tmap, c0 + k * p.boxw, c1, c2);
-                else tma_load_3d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, c2, fb);
-              } else {
-                if (prefetch) tma_prefetch_2d(&p.tmap, c0 + k * p.boxw, c1);
-                else tma_load_2d(dst + k * p.box_slot, &p.tmap, c0 + k * p.boxw, c1, fb);
-              }
-            }
-          };
-          if (it == 0)  // warm the first prefetch window
-            for (int j = 1; j < p.prefetch; ++j)
-              if (t + j * (int)gridDim.x < p.n_tiles) issue(t + j * (int)gridDim.x, true);
-          if (p.prefetch > 0 && t + p.prefetch * (int)gridDim.x < p.n_tiles)
-            issue(t + p.prefetch * (int)gridDim.x, true);
-          SPD_TRACE(0, it);
-          mbar_wait(bar_nate + 8 * ns, nphase ^ 1);  // prefetches go out before the ring wait
+          // select between the two param-space descriptors (a runtime index
+          // into the __grid_constant__ array would copy it to local memory,
+          // where the TMA unit cannot read it)
+          const CUtensorMap* map = (id.step & 1) ? &p.tmap[1] : &p.tmap[0];
           mbar_arrive_expect_tx(fb, box_bytes * p.nbox);
-          issue(t, false);
-          SPD_TRACE(1, it);
+          const int c0 = (int)(p.xoff + id.x0 - 8);
+          const int c1 = (int)(p.yoff + id.y0 - g.r);
+          const int c2 = (int)(p.zoff + id.z0 - g.r);
+          for (int k = 0; k < p.nbox; ++k) {
+            if (g.d == 3) tma_load_3d(dst + k * p.box_slot, map, c0 + k * p.boxw, c1, c2, fb);
+            else tma_load_2d(dst + k * p.box_slot, map, c0 + k * p.boxw, c1, fb);
+          }
         } else {
-          mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
           mbar_arrive_expect_tx(fb, (uint32_t)(g.r_in * C::ROW_BYTES));
-          const T* tbase = in + p.origin + z0 * p.plane + y0 * p.pitch + x0 - 8;
+          const T* in = static_cast<const T*>(p.buf[id.step & 1]);
+          const T* tbase = in + p.origin + id.z0 * p.plane + id.y0 * p.pitch + id.x0 - 8;
           for (int b = 0; b < g.r_in; ++b) {
             const T* src = tbase + (int64_t)g.in_dz[b] * p.plane + (int64_t)g.in_dy[b] * p.pitch + g.in_dx[b];
             bulk_g2s(dst + b * C::ROW_BYTES, src, C::ROW_BYTES, fb);
           }
         }
+        SPD_TRACE(1, it);
       }
     }
   } else if (warp >= kEpiWarps && warp < kMmaWarp) {
@@ -488,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     constexpr int kNW = kNextW + 1;  // next words needed by lane 31
     constexpr int kEW = kPW > kNW ? kPW : kNW;
     int it = 0;
-    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+    for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
       const uint32_t sphase = (it / NSTAGE) & 1;
       const int ns = it % NNAT;
@@ -565,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     // ===================== MMA issuer ======================================
     const uint32_t idesc = idesc_sparse_f16(128, NTILE, std::is_same<T, __nv_bfloat16>::value);
     int it = 0;
-    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+    for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
       const uint32_t sphase = (it / NSTAGE) & 1;
       const int acc = it % NACC;
@@ -599,14 +619,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
     int it = 0;
-    for (int t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++it) {
+    for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       const int acc = it % NACC;
       const uint32_t aphase = (it / NACC) & 1;
-      int64_t z0, y0, x0;
-      tile_origin(t, z0, y0, x0);
-      const int64_t z = z0 + odz;
-      const int64_t y = y0 + ody;
-      const int64_t xr = x0 + odx;  // x of chunk 0 of this row
+      const TileId id = decode(gi);
+      T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
+      const int64_t z = id.z0 + odz;
+      const int64_t y = id.y0 + ody;
+      const int64_t xr = id.x0 + odx;  // x of chunk 0 of this row
       bool row_ok;
       if (g.d == 3) row_ok = z >= p.row_lo && z < p.row_hi && y < p.ny;
       else if (g.d == 2) row_ok = y >= p.row_lo && y < p.row_hi;
@@ -699,6 +719,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         if (cb + 1 < NB) tmem_wait_ld();
       }
       if (warp == 0 && lane == 0) SPD_TRACE(9, it);
+      if (p.steps > 1) {
+        // publish: this tile's stores are complete (epilogue warps only)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (threadIdx.x == 0) {
+          __threadfence();
+          atomicAdd(p.band_done + id.band, 1u);
+        }
+      }
     }
   }
 
@@ -886,10 +914,27 @@ struct spd_plan {
   std::vector<uint32_t> e_words;   // S x 128
   uint16_t* d_a = nullptr;
   uint32_t* d_e = nullptr;
+  unsigned int* d_counters = nullptr;  // per-band completion counters (persistent runs)
+  int counters_cap = 0;
   int sms = 0;
 };
 
 namespace spd {
+
+// Zeroed per-band counters for a persistent launch (stream-ordered memset).
+static int plan_counters(const spd_plan* cplan, int n, cudaStream_t st, unsigned int** out) {
+  spd_plan* plan = const_cast<spd_plan*>(cplan);
+  if (plan->counters_cap < n) {
+    if (plan->d_counters) cudaFree(plan->d_counters);
+    plan->d_counters = nullptr;
+    plan->counters_cap = 0;
+    cudaError_t e = cudaMalloc(&plan->d_counters, sizeof(unsigned int) * n);
+    if (e != cudaSuccess) return cuda_err(e, "counter alloc");
+    plan->counters_cap = n;
+  }
+  *out = plan->d_counters;
+  return cuda_err(cudaMemsetAsync(plan->d_counters, 0, sizeof(unsigned int) * n, st), "counter reset");
+}
 
 template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ, int RIN>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
@@ -915,9 +960,19 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     configured_smem = 232448;
   }
   if (sp.n_tiles <= 0) return SPD_OK;
-  int grid = sp.n_tiles < plan->sms ? sp.n_tiles : plan->sms;
-  kern<<<grid, kThreads, smem, stream>>>(sp);
-  return cuda_err(cudaGetLastError(), "spider_step_kernel launch");
+  const int64_t work = (int64_t)sp.n_tiles * sp.steps;
+  int grid = work < plan->sms ? (int)work : plan->sms;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: cross-step waits need every CTA running
+  attr[0].val.cooperative = sp.steps > 1 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cuda_err(cudaLaunchKernelEx(&cfg, kern, sp), "spider_step_kernel launch");
 }
 
 template <typename T, int PARITY>
@@ -943,7 +998,8 @@ static int dispatch(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
 
 static int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
-static unsigned long long* g_trace = nullptr;  // debug timeline buffer (SPD_TRACE)
+static unsigned long long* g_trace = nullptr;       // debug timeline buffer (SPD_TRACE), device view
+static unsigned long long* g_trace_host = nullptr;  // mapped pinned host view (readable during a hang)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -965,7 +1021,8 @@ static EncodeTiledFn encode_tiled() {
 // Tensor map of an input buffer for the loader warp: the stored grid as a
 // [planes][rows][pitch] (3D) or [rows][pitch] (2D) tensor of 16-bit elements;
 // one box = nbox-th of the tile's halo-padded input block.
-static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const void* buf, StepParams& sp) {
+static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const void* buf, StepParams& sp,
+                           CUtensorMap* map) {
   const Geometry& g = plan->g;
   const int row_elems = g.n_tile * g.L + 16;
   sp.nbox = (row_elems + 255) / 256;
@@ -980,7 +1037,7 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
   cuuint32_t box[3] = {(cuuint32_t)sp.boxw, (cuuint32_t)(g.tile_y + 2 * g.r), (cuuint32_t)(g.tile_z + 2 * g.r)};
   cuuint32_t estr[3] = {1, 1, 1};
   const cuuint32_t rank = g.d == 3 ? 3 : 2;
-  CUresult r = enc(&sp.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, rank, const_cast<void*>(buf), dims, strides, box, estr,
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, rank, const_cast<void*>(buf), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -988,13 +1045,16 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
   return SPD_OK;
 }
 
-static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int64_t lo,
-                            int64_t hi, StepParams& sp) {
+// buf0 holds the input of the launch's first step; steps > 1 alternate buffers
+// inside the (persistent) launch.
+static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const void* buf0, void* buf1, int64_t lo,
+                            int64_t hi, int steps, StepParams& sp) {
   const Geometry& g = plan->g;
   std::memset(&sp, 0, sizeof(sp));
   sp.g = g;
-  sp.in = in;
-  sp.out = out;
+  sp.buf[0] = const_cast<void*>(buf0);
+  sp.buf[1] = buf1;
+  sp.steps = steps;
   sp.pitch = gd->pitch;
   sp.plane = gd->plane;
   sp.origin = gd->origin;
@@ -1027,20 +1087,38 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     sp.tiles_y = sp.tiles_z = 1;
   }
   sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
+  if (g.d == 3) {
+    sp.n_bands = sp.tiles_z;
+    sp.per_band = sp.tiles_x * sp.tiles_y;
+  } else if (g.d == 2) {
+    sp.n_bands = sp.tiles_y;
+    sp.per_band = sp.tiles_x;
+  } else {
+    sp.n_bands = sp.tiles_x;
+    sp.per_band = 1;
+  }
   static const char* dbg_env = getenv("SPD_DBG");
   sp.dbg = dbg_env ? atoi(dbg_env) : 0;
   static const char* pf_env = getenv("SPD_PREFETCH");
   sp.prefetch = pf_env ? atoi(pf_env) : 0;
   sp.trace = nullptr;
   if (getenv("SPD_TRACE")) {
-    if (!g_trace) cudaMalloc(&g_trace, 16 * 64 * sizeof(unsigned long long));
+    if (!g_trace_host) {
+      cudaHostAlloc(&g_trace_host, 8 * 16 * 64 * sizeof(unsigned long long), cudaHostAllocMapped);
+      std::memset(g_trace_host, 0, 8 * 16 * 64 * sizeof(unsigned long long));
+      cudaHostGetDevicePointer(&g_trace, g_trace_host, 0);
+    }
     sp.trace = g_trace;
   }
   sp.zoff = (int)(gd->origin / gd->plane);
   sp.yoff = (int)((gd->origin % gd->plane) / gd->pitch);
   sp.xoff = (int)(gd->origin % gd->pitch);
   sp.use_tmap = 0;
-  if (g.d >= 2) return make_tensor_map(plan, gd, in, sp);
+  if (g.d >= 2) {
+    int rc = make_tensor_map(plan, gd, buf0, sp, &sp.tmap[0]);
+    if (rc) return rc;
+    return make_tensor_map(plan, gd, buf1, sp, &sp.tmap[1]);
+  }
   return SPD_OK;
 }
 
@@ -1126,6 +1204,7 @@ int spd_plan_destroy(spd_plan* plan) {
   if (!plan) return SPD_OK;
   if (plan->d_a) cudaFree(plan->d_a);
   if (plan->d_e) cudaFree(plan->d_e);
+  if (plan->d_counters) cudaFree(plan->d_counters);
   delete plan;
   return SPD_OK;
 }
@@ -1223,26 +1302,44 @@ int spd_step_range(const spd_plan* plan, const spd_grid_desc* gd, const void* in
   int rc = check_desc(plan, gd);
   if (rc) return rc;
   StepParams sp;
-  rc = fill_step_params(plan, gd, in, out, lo, hi, sp);
+  rc = fill_step_params(plan, gd, in, out, lo, hi, 1, sp);
   if (rc) return rc;
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
 
 int spd_run(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* buf1, int steps, void* stream) {
+  static const char* persist_env = getenv("SPD_PERSISTENT");
+  const int flags = (persist_env && atoi(persist_env) != 0) ? SPD_RUN_PERSISTENT : 0;
+  return spd_run_ex(plan, gd, buf0, buf1, steps, flags, stream);
+}
+
+int spd_run_ex(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* buf1, int steps, int flags,
+               void* stream) {
   using namespace spd;
   int rc = check_desc(plan, gd);
   if (rc) return rc;
   if (steps < 1) return set_error(SPD_EINVAL, "step count must be >= 1, got %d", steps);
-  StepParams sp;
-  int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
-  for (int s = 0; s < steps; ++s) {
-    rc = fill_step_params(plan, gd, s % 2 ? buf1 : buf0, s % 2 ? buf0 : buf1, 0, extent, sp);
+  // Default: one launch per step (alternating traversal for L2 reuse).
+  // SPD_RUN_PERSISTENT: one cooperative launch for all steps, ordered by
+  // per-band completion counters (correct, currently slower: the per-tile
+  // publish fence costs more than the launch boundaries it removes; see
+  // DESIGN.md §7).
+  const bool persistent = (flags & SPD_RUN_PERSISTENT) != 0;
+  const int64_t extent = plan->d == 3 ? gd->nz : (plan->d == 2 ? gd->ny : 1);
+  int done = 0;
+  while (done < steps) {
+    const int chunk = persistent ? (steps - done > 100000 ? 100000 : steps - done) : 1;
+    StepParams sp;
+    rc = fill_step_params(plan, gd, done % 2 ? buf1 : buf0, done % 2 ? buf0 : buf1, 0, extent, chunk, sp);
     if (rc) return rc;
-    // Alternate the traversal direction: step s+1 starts on the tiles step s
-    // wrote last, which are still resident in the 126 MB L2.
-    sp.reverse = s & 1;
+    if (chunk > 1) {
+      rc = plan_counters(plan, sp.n_bands, (cudaStream_t)stream, &sp.band_done);
+      if (rc) return rc;
+    }
+    sp.reverse = persistent ? 0 : (done & 1);
     rc = dispatch(plan, sp, (cudaStream_t)stream);
     if (rc) return rc;
+    done += chunk;
   }
   return SPD_OK;
 }
@@ -1351,8 +1448,9 @@ int spd_naive_apply_f64(int d, int r, const double* coeffs, int64_t nz, int64_t 
 
 // Debug: copy the CTA-0 timeline of the last traced launch (16 x 64 stamps).
 extern "C" int spd_debug_trace(unsigned long long* host) {
-  if (!spd::g_trace) return spd::set_error(SPD_EINVAL, "no trace (set SPD_TRACE and run a step)");
-  return spd::cuda_err(cudaMemcpy(host, spd::g_trace, 16 * 64 * 8, cudaMemcpyDeviceToHost), "trace copy");
+  if (!spd::g_trace_host) return spd::set_error(SPD_EINVAL, "no trace (set SPD_TRACE and run a step)");
+  std::memcpy(host, spd::g_trace_host, 8 * 16 * 64 * 8);  // mapped memory: readable while a kernel runs
+  return SPD_OK;
 }
 
 int spd_mma_selftest(const uint16_t* a, const uint8_t* e, const uint16_t* b, int n, float* d, void* stream) {

@@ -119,11 +119,12 @@ class SlabDriver:
         return [(0, band), (rows - band, rows)], [(band, rows - band)]
 
     def step(self) -> None:
+        """One timestep: boundary bands, exchange (overlapped on the comm
+        stream when CUDA), interior bands, flip."""
         boundary, interior = self._bands()
-        cuda = self.comm_stream is not None
         for lo, hi in boundary:
             self.ops.compute(lo, hi)
-        if cuda:
+        if self.comm_stream is not None:
             done = torch.cuda.Event()
             done.record(self.compute_stream)
             with torch.cuda.stream(self.comm_stream):
@@ -140,17 +141,43 @@ class SlabDriver:
                 self.ops.compute(lo, hi)
         self.ops.flip()
 
-    def _exchange(self) -> None:
+    # phase API (used to emulate several ranks in one process)
+    def step_boundary(self) -> None:
+        for lo, hi in self._bands()[0]:
+            self.ops.compute(lo, hi)
+
+    def pack_messages(self) -> None:
         m, s = self.msgs, self.slab
         if s.up is not None:
             self.ops.pack("up", m["send_up"])
         if s.down is not None:
             self.ops.pack("down", m["send_down"])
-        exchange(s, m["send_up"], m["send_down"], m["recv_up"], m["recv_down"], self.group)
+
+    def unpack_messages(self) -> None:
+        m, s = self.msgs, self.slab
         if s.up is not None:
             self.ops.unpack("up", m["recv_up"])
         if s.down is not None:
             self.ops.unpack("down", m["recv_down"])
+
+    def step_interior_and_flip(self) -> None:
+        for lo, hi in self._bands()[1]:
+            self.ops.compute(lo, hi)
+        self.ops.flip()
+
+    def _exchange(self) -> None:
+        m, s = self.msgs, self.slab
+        self.pack_messages()
+        exchange(s, m["send_up"], m["send_down"], m["recv_up"], m["recv_down"], self.group)
+        self.unpack_messages()
+
+
+def local_exchange(drivers) -> None:
+    """Exchange halos between SlabDrivers living in one process (ranks
+    emulated on one device): rank k's send_down -> rank k+1's recv_up etc."""
+    for a, b in zip(drivers, drivers[1:]):
+        b.msgs["recv_up"].copy_(a.msgs["send_down"])
+        a.msgs["recv_down"].copy_(b.msgs["send_up"])
 
 
 class DeviceSlabOps(SlabOps):
@@ -188,4 +215,4 @@ class DeviceSlabOps(SlabOps):
                                   0 if which == "up" else 1, C.c_void_p(msg.data_ptr()), _stream_ptr()))
 
 
-__all__ = ["Slab", "decompose", "exchange", "SlabOps", "SlabDriver", "DeviceSlabOps"]
+__all__ = ["Slab", "decompose", "exchange", "local_exchange", "SlabOps", "SlabDriver", "DeviceSlabOps"]

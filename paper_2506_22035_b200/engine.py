@@ -176,13 +176,14 @@ class DeviceGrid:
         check(lib.spd_download(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
                                C.c_void_p(host.data_ptr()), _stream_ptr(stream)))
 
-    def run(self, steps: int, stream=None) -> None:
-        """`steps` Jacobi steps on the device, ping-ponging the buffers."""
+    def run(self, steps: int, stream=None, persistent: bool = False) -> None:
+        """`steps` Jacobi steps on the device, ping-ponging the buffers
+        (one launch per step, or one persistent launch)."""
         if steps < 1:
             raise ValueError(f"step count must be >= 1, got {steps}")
         a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
-        check(lib.spd_run(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                          int(steps), _stream_ptr(stream)))
+        check(lib.spd_run_ex(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                             int(steps), 1 if persistent else 0, _stream_ptr(stream)))
         self.cur = (self.cur + steps) % 2
         self.step += steps
 

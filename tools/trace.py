@@ -14,9 +14,9 @@ plan = get_plan(bench.make_kernel(kind, d, r), sp.Parity.EVEN, "fp16")
 g = DeviceGrid(plan, shape, r)
 g.load_dense_f64(torch.rand(g.dense_shape, dtype=torch.float64, device="cuda") - 0.5)
 g.run(4); torch.cuda.synchronize()
-buf = (C.c_ulonglong * (16 * 64))()
+buf = (C.c_ulonglong * (8 * 16 * 64))()
 assert _lib.lib.spd_debug_trace(buf) == 0
-a = np.array(buf, dtype=np.int64).reshape(16, 64)
+a = np.array(buf, dtype=np.int64).reshape(8, 16, 64)[0]
 names = ["ld_wait", "ld_issued", "pr_natfull", "pr_bempty", "pr0_done", "pr7_done", "mma_accfree", "mma_issue", "epi_start", "epi_done"]
 t0 = a[13, 0]
 print(f"entry->setup done {(a[14,0]-a[13,0])/1965:.2f} us, entry->exit {(a[15,0]-a[13,0])/1965:.2f} us, first load issued {(a[1,0]-a[13,0])/1965:.2f} us, first epi done {(a[9,0]-a[13,0])/1965:.2f} us")
