@@ -204,15 +204,21 @@ int build_geometry(int d, int r, Geometry* g) {
   std::memset(g, 0, sizeof(*g));
   int L = band_rows(r);
   if (L < 0) return L;
-  if (L != 4 && L != 8)
+  if (L > 16)
     return set_error(SPD_EUNSUPPORTED,
-                     "unsupported radius %d for the device path (supported: r in {1, 3})", r);
+                     "unsupported radius %d for the device path (supported: 1 <= r <= 7)", r);
   if (d == 3 && L != 4)
     return set_error(SPD_EUNSUPPORTED, "unsupported radius %d for 3D on the device (r = 1 only)", r);
   g->d = d;
   g->r = r;
   g->L = L;
-  g->kc = 2 * L / 8;
+  // window of 2L slots in 16-byte K-chunks; a K=32 MMA holds 4 chunks, so the
+  // per-row chunk count is padded to a divisor of 4 (pad slots carry zero
+  // coefficients with (0,1) metadata)
+  {
+    const int need = (2 * L + 7) / 8;
+    g->kc = need <= 1 ? 1 : (need <= 2 ? 2 : 4);
+  }
   g->rows_per_mma = 4 / g->kc;
   g->r_out = 128 / L;
   int rin = 0;
@@ -333,7 +339,7 @@ int pack_operands(const Geometry& g, int n_rows, const double* row_values,
         for (int i = 0; i < L; ++i) {
           int m = L * a + i;
           for (int sg = 0; sg < segs_per_row; ++sg) {
-            int kseg = c * segs_per_row + sg;  // segment within K=32
+            int kseg = c * 2 * g.kc + sg;  // segment within K=32 (rows padded to kc chunks)
             for (int t = 0; t < 2; ++t) {
               double v = vals[i * L + 2 * sg + t];
               a_img[((size_t)s * 128 + m) * 16 + 2 * kseg + t] =

@@ -145,6 +145,10 @@ __device__ __forceinline__ void tmem_wait_st() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                        uint32_t d) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
@@ -221,13 +225,24 @@ constexpr int kThreads = 32 * (kLoadWarp + 1);
 
 template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
 struct Cfg {
-  static constexpr int KC = 2 * L / 8;
-  static constexpr int CPL = 8 / L;          // chunks per lane per 16-B word group
+  // fast paths: L = 4 (r = 1) and L = 8 (r = 3); any other even L up to 16 uses
+  // the generic producer / epilogue
+  static constexpr bool GEN = !(L == 4 || L == 8);
+  static constexpr int KC = (2 * L + 7) / 8 <= 1 ? 1 : ((2 * L + 7) / 8 <= 2 ? 2 : 4);
+  static constexpr int CPL = GEN ? 1 : 8 / L;  // chunks per lane
   static constexpr int SEG = 32 * CPL;       // chunks per warp segment (256 points)
   static constexpr int SEGS = NTILE / SEG;   // segments per tile row
   // natural row segment staged by the bulk copy: [x0 - 8, x0 + NTILE*L + 8)
   static constexpr int ROW_ELEMS = NTILE * L + 16;
   static constexpr int ROW_BYTES = ROW_ELEMS * 2;
+  // tensor-TMA split of the natural row into NBOX boxes of BOXW (<= 256) elements
+  static constexpr int NBOX = (ROW_ELEMS + 255) / 256;
+  static constexpr int BOXW = ((ROW_ELEMS + NBOX - 1) / NBOX + 7) / 8 * 8;
+  // generic epilogue staging: rows of 32*L points with a pitch of 66L bytes
+  // (== 2L mod 128, so consecutive TMEM lanes hit consecutive banks)
+  static constexpr int R_OUT = 128 / L;
+  static constexpr int STG_PITCH = 66 * L;
+  static constexpr int STG_BYTES = GEN ? 2 * R_OUT * STG_PITCH : 0;
   static constexpr int ACC_COL = 0;
   static constexpr int E_COL = NACC * NTILE;
   // E for MMA s at E_COL + 2s: bit 0 of the metadata TMEM address is the
@@ -318,7 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   const int stage_bytes = (NTILE / 8) * sbo;
   uint8_t* bimg = smem;
   uint8_t* nat = smem + NSTAGE * stage_bytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(nat + NNAT * p.nat_bytes);
+  uint8_t* stg = nat + NNAT * p.nat_bytes;  // generic epilogue staging (C::STG_BYTES)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + C::STG_BYTES);
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC + 2 * NNAT);
   const uint32_t bimg_s = smem_u32(bimg);
   const uint32_t nat_s = smem_u32(nat);
@@ -465,6 +481,68 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
   } else if (warp >= kEpiWarps && warp < kMmaWarp) {
     // ===================== producer: natural rows -> permuted B image =====
+    if constexpr (C::GEN) {
+      // Generic radius (L = 2r+2 not in {4, 8}): one chunk per lane; the lane
+      // reads its 2L-point window as 32-bit words straight from the natural
+      // stage and permutes it with compile-time PRMT selectors; window slots
+      // past 2L (K-chunk padding) are zero.
+      const int pw = warp - kEpiWarps;
+      constexpr int R = (L - 2) / 2;
+      constexpr int n_items = RIN * C::SEGS;
+      static_assert((NQ - 1) * kProdWarps < n_items && NQ * kProdWarps >= n_items, "NQ must cover the items");
+      constexpr int OFF = R & 1;                  // window-start parity (n*L is even)
+      constexpr int NW = (OFF + 2 * L + 1) / 2;  // natural words covering one window
+      int it = 0;
+      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+        const int stage = it % NSTAGE;
+        const uint32_t sphase = (it / NSTAGE) & 1;
+        const int ns = it % NNAT;
+        const uint32_t nphase = (it / NNAT) & 1;
+        const uint32_t nbase = nat_s + ns * p.nat_bytes;
+        mbar_wait(bar_natf + 8 * ns, nphase);
+        mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
+        const uint32_t sbase = bimg_s + stage * stage_bytes;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int item = pw + q * kProdWarps;
+          if (q == NQ - 1 && item >= n_items) continue;
+          const int b = item / C::SEGS, sg = item % C::SEGS;
+          const int n = sg * 32 + lane;
+          const int s_al = n * L - R + 8 - OFF;
+          uint32_t w[NW];
+#pragma unroll
+          for (int k = 0; k < NW; ++k) {
+            const int e = s_al + 2 * k;
+            // tensor-TMA stage: [box][row][BOXW]; 1D bulk stage: [row][ROW_ELEMS]
+            const int kb = p.use_tmap ? e / C::BOXW : 0;
+            const int bw = p.use_tmap ? C::BOXW : C::ROW_ELEMS;
+            w[k] = lds_u32(nbase + kb * p.box_slot + (b * bw + e - kb * bw) * 2);
+          }
+          const uint32_t gbase = sbase + (n / 8) * sbo + (n % 8) * 16 + b * KC * 128;
+#pragma unroll
+          for (int kc = 0; kc < KC; ++kc) {
+            uint32_t wd[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int q0 = 8 * kc + 2 * u;
+              if (q0 < 2 * L) {
+                const int e0 = OFF + perm_slot(L, PARITY, q0), e1 = OFF + perm_slot(L, PARITY, q0 + 1);
+                wd[u] = __byte_perm(w[e0 / 2], w[e1 / 2], sel_halves(e0 % 2, e1 % 2));
+              } else {
+                wd[u] = 0u;
+              }
+            }
+            sts_v4(gbase + kc * 128, wd[0], wd[1], wd[2], wd[3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bar_nate + 8 * ns);
+          mbar_arrive(bar_full + 8 * stage);
+        }
+      }
+    } else {
     const int pw = warp - kEpiWarps;
     constexpr int n_items = RIN * C::SEGS;
     static_assert((NQ - 1) * kProdWarps < n_items && NQ * kProdWarps >= n_items, "NQ must cover the items");
@@ -581,6 +659,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         if (pw == kProdWarps - 1) SPD_TRACE(5, it);
       }
     }
+    }
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer ======================================
     const uint32_t idesc = idesc_sparse_f16(128, NTILE, std::is_same<T, __nv_bfloat16>::value);
@@ -612,6 +691,82 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
   } else {
     // ===================== epilogue ========================================
+    if constexpr (C::GEN) {
+      // Generic radius: TMEM lane m = L*alpha + i.  Lane pairs (i, i+1) pack
+      // their fp16 values through a shuffle, store 32-bit words into a staging
+      // tile [alpha][32*L points] (pitch 66L bytes: consecutive lanes hit
+      // consecutive banks), and the four epilogue warps then copy the tile out
+      // with coalesced 32-bit stores.  Two staging buffers, one named barrier
+      // per batch.
+      constexpr int NB = NTILE / 32;
+      const int quad = warp;
+      const int m = quad * 32 + lane;
+      const int alpha = m / L;
+      const int i = m - alpha * L;
+      const bool lead = alpha < C::R_OUT && (i % 2) == 0;
+      const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+      const uint32_t stg_s = smem_u32(stg);
+      int bt = 0;
+      int it = 0;
+      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+        const int acc = it % NACC;
+        const uint32_t aphase = (it / NACC) & 1;
+        const TileId id = decode(gi);
+        T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
+        mbar_wait(bar_accf + 8 * acc, aphase);
+        tc_fence_after();
+        const uint32_t tcol = lane_base + C::ACC_COL + acc * NTILE;
+        uint32_t va[32], vb[32];
+        tmem_ld_x32(tcol, va);
+        tmem_wait_ld();
+#pragma unroll
+        for (int cb = 0; cb < NB; ++cb, ++bt) {
+          uint32_t(&v)[32] = (cb & 1) ? vb : va;
+          uint32_t(&vn)[32] = (cb & 1) ? va : vb;
+          if (cb + 1 < NB) tmem_ld_x32(tcol + (cb + 1) * 32, vn);
+          if (cb == NB - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
+          }
+          const uint32_t sb = stg_s + (bt & 1) * (C::R_OUT * C::STG_PITCH);
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            const uint32_t mine = Cvt<T>::pack(__uint_as_float(v[2 * jj]), __uint_as_float(v[2 * jj + 1]));
+            const uint32_t nb = __shfl_down_sync(0xffffffffu, mine, 1);  // lane (alpha, i+1)
+            if (lead) {
+              const uint32_t row = sb + alpha * C::STG_PITCH;
+              sts_u32(row + ((2 * jj) * L + i) * 2, __byte_perm(mine, nb, 0x5410));
+              sts_u32(row + ((2 * jj + 1) * L + i) * 2, __byte_perm(mine, nb, 0x7632));
+            }
+          }
+          asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
+          // coalesced copy-out of R_OUT rows x 16L words
+          constexpr int WPR = 16 * L;
+          for (int wi = threadIdx.x; wi < C::R_OUT * WPR; wi += 32 * kEpiWarps) {
+            const int row = wi / WPR;
+            const int col = wi - row * WPR;
+            const int64_t z = id.z0 + g.out_dz[row];
+            const int64_t y = id.y0 + g.out_dy[row];
+            const int64_t x = id.x0 + g.out_dx[row] + (int64_t)cb * 32 * L + 2 * col;
+            bool ok = x < p.nx;
+            if (g.d == 2) ok = ok && y >= p.row_lo && y < p.row_hi;
+            if (ok && !(p.dbg & 1)) {
+              const uint32_t val = lds_u32(sb + row * C::STG_PITCH + col * 4);
+              *reinterpret_cast<uint32_t*>(out + p.origin + z * p.plane + y * p.pitch + x) = val;
+            }
+          }
+          if (cb + 1 < NB) tmem_wait_ld();
+        }
+        if (p.steps > 1) {
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+          if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(p.band_done + id.band, 1u);
+          }
+        }
+      }
+    } else {
     const int quad = warp;  // TMEM lane quadrant
     const int m = quad * 32 + lane;  // TMEM lane == M row
     const int alpha = m / L;         // output row of the tile
@@ -727,6 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           atomicAdd(p.band_done + id.band, 1u);
         }
       }
+    }
     }
   }
 
@@ -947,7 +1103,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     sp.boxw = C::ROW_ELEMS;
     sp.box_slot = sp.nat_bytes;
   }
-  const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + (size_t)NNAT * sp.nat_bytes +
+  const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + (size_t)NNAT * sp.nat_bytes + C::STG_BYTES +
                       8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT) + 16;
   if (smem > 232448) return set_error(SPD_EUNSUPPORTED, "shared memory budget exceeded (%zu B)", smem);
   if (C::A_COL + 8 * plan->g.s > 512) return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
@@ -986,6 +1142,17 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   if (g.L == 4 && g.n_tile == 64 && g.r_in == 60) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 8, 60>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 6, 22>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 4, 16>(plan, sp, st);
+  // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
+  if (g.L == 6 && g.r_in == 25) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 7, 25>(plan, sp, st);
+  if (g.L == 6 && g.r_in == 21) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 6, 21>(plan, sp, st);
+  if (g.L == 10 && g.r_in == 20) return launch_step<T, 10, PARITY, 64, 2, 1, 4, 5, 20>(plan, sp, st);
+  if (g.L == 10 && g.r_in == 12) return launch_step<T, 10, PARITY, 64, 2, 2, 4, 3, 12>(plan, sp, st);
+  if (g.L == 12 && g.r_in == 20) return launch_step<T, 12, PARITY, 64, 2, 1, 4, 5, 20>(plan, sp, st);
+  if (g.L == 12 && g.r_in == 10) return launch_step<T, 12, PARITY, 64, 2, 2, 4, 3, 10>(plan, sp, st);
+  if (g.L == 14 && g.r_in == 21) return launch_step<T, 14, PARITY, 64, 2, 1, 4, 6, 21>(plan, sp, st);
+  if (g.L == 14 && g.r_in == 9) return launch_step<T, 14, PARITY, 64, 2, 2, 4, 3, 9>(plan, sp, st);
+  if (g.L == 16 && g.r_in == 22) return launch_step<T, 16, PARITY, 64, 1, 1, 4, 6, 22>(plan, sp, st);
+  if (g.L == 16 && g.r_in == 8) return launch_step<T, 16, PARITY, 64, 2, 2, 4, 2, 8>(plan, sp, st);
   return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
 }
 
@@ -1024,10 +1191,11 @@ static EncodeTiledFn encode_tiled() {
 static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const void* buf, StepParams& sp,
                            CUtensorMap* map) {
   const Geometry& g = plan->g;
+  // same split as Cfg::NBOX / Cfg::BOXW: <= 256-element boxes, widths a
+  // multiple of 8 (boxes may overrun the row; TMA zero-fills out of bounds)
   const int row_elems = g.n_tile * g.L + 16;
   sp.nbox = (row_elems + 255) / 256;
-  sp.boxw = row_elems / sp.nbox;
-  if (row_elems % sp.nbox || sp.boxw % 8) return set_error(SPD_EUNSUPPORTED, "bad TMA box split (%d)", row_elems);
+  sp.boxw = ((row_elems + sp.nbox - 1) / sp.nbox + 7) / 8 * 8;
   sp.box_slot = (int)roundup((int64_t)sp.boxw * 2 * g.r_in, 128);
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");

@@ -11,7 +11,7 @@
 #define SPD_ABI_VERSION 1
 #define SPD_MAX_RIN 64
 #define SPD_MAX_ROUT 32
-#define SPD_MAX_S 16
+#define SPD_MAX_S 24
 
 namespace spd {
 
@@ -36,7 +36,7 @@ uint16_t f64_to_bf16_bits(double x);
 // Passed to the kernel by value.
 struct Geometry {
   int d, r, L;
-  int kc;            // 16-byte K-chunks per input-row window (2L/8)
+  int kc;            // 16-byte K-chunks per input-row window (2L/8 rounded up to 1, 2 or 4)
   int rows_per_mma;  // input rows per K=32 MMA (4/kc)
   int r_out;         // output rows per tile (128/L)
   int r_in;          // input image rows per tile

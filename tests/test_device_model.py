@@ -49,7 +49,8 @@ def tile_model(plan, dense, halo):
     A = decode_A(a_img, e_words)
     dense3 = dense if dense.ndim == 3 else dense[None]
     zh = halo if dense.ndim == 3 else 0
-    Bimg = np.zeros((inf.r_in, n_tile, 2 * L))
+    kslots = 8 * inf.kchunks  # window slots per input row (2L padded with zeros)
+    Bimg = np.zeros((inf.r_in, n_tile, kslots))
     for b in range(inf.r_in):
         dz, dy, dx = in_off[b]
         for n in range(n_tile):
@@ -58,7 +59,7 @@ def tile_model(plan, dense, halo):
                 zz, yy, xx = dz + zh, dy + halo, x + halo
                 if 0 <= zz < dense3.shape[0] and 0 <= yy < dense3.shape[1] and 0 <= xx < dense3.shape[2]:
                     Bimg[b, n, q] = dense3[zz, yy, xx]
-    rpm = 32 // (2 * L)
+    rpm = 32 // kslots
     D = np.zeros((128, n_tile))
     for s in range(inf.mmas_per_tile):
         Bs = Bimg[starts[s] : starts[s] + rpm].transpose(0, 2, 1).reshape(32, n_tile)
@@ -84,6 +85,15 @@ CASES = [
     ("box", 3, 1),
     ("box", 1, 1),
     ("box", 1, 3),
+    # generic radii (padded K-chunks, R_out = 128 // L)
+    ("box", 2, 2),
+    ("star", 2, 2),
+    ("box", 2, 4),
+    ("box", 2, 5),
+    ("box", 2, 6),
+    ("box", 2, 7),
+    ("box", 1, 2),
+    ("box", 1, 5),
 ]
 
 
@@ -141,6 +151,9 @@ def test_bf16_operands():
 
 
 def test_unsupported_radius_rejected_by_device_plan():
-    k = sp.make_kernel("box", 2, 2, np.ones(25))
+    k = sp.make_kernel("box", 2, 8, np.ones(17 * 17))
     with pytest.raises(ValueError, match="unsupported"):
         Plan(k, "even", "fp16", device=-1)
+    k3 = sp.make_kernel_3d("box", 2, np.ones(125))
+    with pytest.raises(ValueError, match="unsupported"):
+        Plan(k3, "even", "fp16", device=-1)

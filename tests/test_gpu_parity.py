@@ -127,6 +127,15 @@ def test_s5_oracle_config(golden):
     ("star", 3, 1, (4, 8, 256)),
     ("box", 1, 1, (1, 1000)),
     ("box", 1, 3, (1, 16384 + 40)),
+    # generic radii (L = 2r+2 not in {4, 8})
+    ("box", 2, 2, (50, 390)),
+    ("star", 2, 2, (64, 768)),
+    ("box", 2, 4, (30, 700)),
+    ("box", 2, 5, (25, 840)),
+    ("box", 2, 6, (20, 1064)),
+    ("star", 2, 7, (17, 1024)),
+    ("box", 1, 2, (1, 9000)),
+    ("box", 1, 5, (1, 12000)),
 ])
 @pytest.mark.parametrize("parity", ["even", "odd"])
 def test_execute_matches_oracle(shape, d, r, dims, parity):
@@ -148,13 +157,14 @@ def test_execute_matches_oracle(shape, d, r, dims, parity):
         np.testing.assert_array_equal(got.data[mask], grid.data[mask])
 
 
-@pytest.mark.parametrize("d,r", [(2, 1), (2, 3), (3, 1), (1, 1)])
+@pytest.mark.parametrize("d,r", [(2, 1), (2, 3), (3, 1), (1, 1), (2, 2), (2, 7), (1, 4)])
 def test_single_step_within_one_fp16_rounding(d, r):
     """One step, fp16-rounded coefficients in the oracle: the device result is
     the fp16 rounding of an fp32-accumulated exact sum."""
     k = rand_kernel("box", d, r, seed=[d, r, 77])
     kq = quant(k.coeffs)
-    dims = {1: (1, 4096), 2: (40, 520), 3: (8, 16, 256)}[d]
+    L = 2 * r + 2
+    dims = {1: (1, 96 * L * 16), 2: (40, 64 * L * 2 + 8 * L), 3: (8, 16, 256)}[d]
     got, _, grid, _ = run_case(k, dims, 1, seed=4)
     want = cnaive.naive_apply(kq, d, r, grid.data, r, 1)
     h = r
@@ -251,12 +261,13 @@ def test_reference_error_contract():
     k = sp.make_kernel("box", 2, 2, np.ones(25))
     with pytest.raises(ValueError, match="multiple"):
         sp.execute(k, sp.random_grid(32, 32, 2, seed=0), 1)  # 32 % L=6 != 0
+    k8 = sp.make_kernel("box", 2, 8, np.ones(17 * 17))
     with pytest.raises(ValueError, match="halo"):
         sp.execute(rand_kernel("box", 2, 3, 0), sp.random_grid(32, 32, 1, seed=0), 1)
     with pytest.raises(ValueError, match="step"):
         sp.execute(rand_kernel("box", 2, 1, 0), sp.random_grid(32, 32, 1, seed=0), 0)
     with pytest.raises(ValueError, match="unsupported"):
-        sp.execute(k, sp.random_grid(32, 36, 2, seed=0), 1)
+        sp.execute(k8, sp.random_grid(36, 36, 8, seed=0), 1)
 
 
 def test_verify_report():

@@ -29,3 +29,9 @@ bench("Box-2D49P 10240^2", sp.make_kernel("box",2,3,w), (10240,10240))
 w = rng.uniform(0.5,1.5,27); w/=w.sum()
 bench("Box-3D27P 512^3", sp.make_kernel_3d("box",1,w), (512,512,512))
 bench("Heat-2D 16384^2", sp.make_kernel("star",2,1,c), (16384,16384))
+if len(sys.argv) > 1 and sys.argv[1] == "generic":
+    for r in (2, 4, 7):
+        n = 2 * r + 1
+        w = rng.uniform(0.5, 1.5, n * n); w /= w.sum()
+        L = 2 * r + 2
+        bench(f"Box-2D{n*n}P r={r} ~10240^2", sp.make_kernel("box", 2, r, w), (10240, (10240 // (64 * L)) * 64 * L))
