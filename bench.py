@@ -1,6 +1,6 @@
 """Benchmark of the SPIDER hot path on B200 (contract: see DESIGN.md §Measurement).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config B9|B49|B27|W|S5]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config B9|B49|B27|B25|W|S5]
                     [--impl ours|reference] [--no-cpu-baseline]
 
 One bench "step" = one pass of the configuration over its grid: T Jacobi
@@ -35,6 +35,8 @@ CONFIGS = {
     "B9": ("Box-2D9P fp16 10240x10240, 100 timesteps", (10240, 10240), 2, 1, "box", 100),
     "B49": ("Box-2D49P (7x7) fp16 10240x10240, 100 timesteps", (10240, 10240), 2, 3, "box", 100),
     "B27": ("Box-3D27P fp16 512^3, 100 timesteps", (512, 512, 512), 3, 1, "box", 100),
+    # the paper's Box-2D2R ablation stencil; width a multiple of L = 6
+    "B25": ("Box-2D25P (5x5) fp16 10240x10242, 100 timesteps", (10240, 10242), 2, 2, "box", 100),
     "W": ("Box-2D9P fp16 16384x16384 per GPU, 100 timesteps", (16384, 16384), 2, 1, "box", 100),
 }
 

@@ -238,11 +238,12 @@ struct Cfg {
   // tensor-TMA split of the natural row into NBOX boxes of BOXW (<= 256) elements
   static constexpr int NBOX = (ROW_ELEMS + 255) / 256;
   static constexpr int BOXW = ((ROW_ELEMS + NBOX - 1) / NBOX + 7) / 8 * 8;
-  // generic epilogue staging: rows of 32*L points with a pitch of 66L bytes
-  // (== 2L mod 128, so consecutive TMEM lanes hit consecutive banks)
+  // generic epilogue staging: rows of 32*L points (64L bytes) with a 16-byte
+  // pad: rows stay 16-B aligned for the vector copy-out and successive rows
+  // start 4 banks apart
   static constexpr int R_OUT = 128 / L;
-  static constexpr int STG_PITCH = 66 * L;
-  static constexpr int STG_BYTES = GEN ? 2 * R_OUT * STG_PITCH : 0;
+  static constexpr int STG_PITCH = 64 * L + 16;
+  static constexpr int STG_BYTES = GEN ? 2 * R_OUT * STG_PITCH + 16 * R_OUT + 16 : 0;
   static constexpr int ACC_COL = 0;
   static constexpr int E_COL = NACC * NTILE;
   // E for MMA s at E_COL + 2s: bit 0 of the metadata TMEM address is the
@@ -706,6 +707,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       const bool lead = alpha < C::R_OUT && (i % 2) == 0;
       const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
       const uint32_t stg_s = smem_u32(stg);
+      // per-row output offsets relative to the tile origin (loop-invariant),
+      // kept in the tail of the staging area: {offset, dy}
+      int64_t* rowtab = reinterpret_cast<int64_t*>(stg + 2 * C::R_OUT * C::STG_PITCH);
+      if (threadIdx.x < C::R_OUT) {
+        const int rr = threadIdx.x;
+        rowtab[2 * rr] = (int64_t)g.out_dz[rr] * p.plane + (int64_t)g.out_dy[rr] * p.pitch + g.out_dx[rr];
+        rowtab[2 * rr + 1] = ((int64_t)g.out_dy[rr] << 32) | (uint32_t)g.out_dx[rr];
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
       int bt = 0;
       int it = 0;
       for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
@@ -741,19 +751,29 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             }
           }
           asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
-          // coalesced copy-out of R_OUT rows x 16L words
-          constexpr int WPR = 16 * L;
-          for (int wi = threadIdx.x; wi < C::R_OUT * WPR; wi += 32 * kEpiWarps) {
-            const int row = wi / WPR;
-            const int col = wi - row * WPR;
-            const int64_t z = id.z0 + g.out_dz[row];
-            const int64_t y = id.y0 + g.out_dy[row];
-            const int64_t x = id.x0 + g.out_dx[row] + (int64_t)cb * 32 * L + 2 * col;
-            bool ok = x < p.nx;
-            if (g.d == 2) ok = ok && y >= p.row_lo && y < p.row_hi;
-            if (ok && !(p.dbg & 1)) {
-              const uint32_t val = lds_u32(sb + row * C::STG_PITCH + col * 4);
-              *reinterpret_cast<uint32_t*>(out + p.origin + z * p.plane + y * p.pitch + x) = val;
+          // coalesced copy-out of R_OUT rows x 4L 16-byte vectors
+          constexpr int VPR = 4 * L;
+          T* tbase = out + p.origin + id.z0 * p.plane + id.y0 * p.pitch + id.x0 + (int64_t)cb * 32 * L;
+          const int64_t xlim = p.nx - id.x0 - (int64_t)cb * 32 * L;
+          for (int vi = threadIdx.x; vi < C::R_OUT * VPR; vi += 32 * kEpiWarps) {
+            const int row = vi / VPR;
+            const int col = vi - row * VPR;
+            const int64_t roff = rowtab[2 * row];
+            const int64_t rdy = rowtab[2 * row + 1];
+            const int dy = (int)(rdy >> 32), dx = (int)(uint32_t)rdy;
+            const int64_t y = id.y0 + dy;
+            bool ok = true;
+            if (g.d == 2) ok = y >= p.row_lo && y < p.row_hi;
+            const int64_t x = dx + 8 * col;  // first of the vector's 8 points
+            if (ok && x < xlim && !(p.dbg & 1)) {
+              const uint4 val = lds_v4(sb + row * C::STG_PITCH + col * 16);
+              T* dst = tbase + roff + 8 * col;
+              if (x + 8 <= xlim) {
+                *reinterpret_cast<uint4*>(dst) = val;
+              } else {  // ragged right edge: whole 32-bit pairs only (nx is even)
+                const uint32_t wv[4] = {val.x, val.y, val.z, val.w};
+                for (int k = 0; k < 4 && x + 2 * k < xlim; ++k) reinterpret_cast<uint32_t*>(dst)[k] = wv[k];
+              }
             }
           }
           if (cb + 1 < NB) tmem_wait_ld();
