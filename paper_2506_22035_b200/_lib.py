@@ -88,7 +88,7 @@ SIGNATURES = {
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_2506_22035_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_2506_22035_b200/build.py` "
             "(or __graft_entry__.build()); there is no fallback path"
         )
     lib = C.CDLL(str(LIB_PATH))
