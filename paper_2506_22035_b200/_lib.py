@@ -12,7 +12,8 @@ from pathlib import Path
 import numpy as np
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libspider.so"
+# SPD_LIB: development override (A/B timing of two builds); default in-tree
+LIB_PATH = Path(os.environ["SPD_LIB"]) if os.environ.get("SPD_LIB") else _HERE / "libspider.so"
 
 SPD_OK = 0
 SPD_EINVAL = -1

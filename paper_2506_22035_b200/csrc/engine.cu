@@ -24,7 +24,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <type_traits>
 #include <vector>
 
@@ -111,6 +113,21 @@ __device__ __forceinline__ void mma_sp_ts(uint32_t d, uint32_t a, uint64_t bdesc
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%3], %5, p;\n}\n" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(e), "r"(accum), "r"(idesc));
+}
+
+// Same, issued by one elected lane of a converged warp.
+__device__ __forceinline__ void mma_sp_ts_elect(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t e, uint32_t idesc,
+                                                uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|q, 0xffffffff;\n"
+      "@q tcgen05.mma.sp.cta_group::1.kind::f16 [%0], [%1], %2, [%3], %5, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(e), "r"(accum), "r"(idesc));
+}
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .pred q;\nelect.sync _|q, 0xffffffff;\n"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(bar)
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_st_x1(uint32_t taddr, uint32_t v) {
@@ -202,6 +219,13 @@ struct StepParams {
   int steps;                 // Jacobi steps in this launch (persistent, >= 1)
   unsigned int* band_done;   // [n_bands] completed tiles per band (steps > 1)
   int per_band, n_bands;     // tiles per band; bands (2D: tile rows, 3D: tile planes, 1D: tiles)
+  // persistent (steps > 1) work order: sweeps of `sweep` steps; inside a
+  // sweep, wavefront w holds (local step s, band w - lag*s) for s ascending,
+  // so step s+1 trails step s by `lag` bands and reads what step s wrote a
+  // few wavefronts earlier, still resident in L2 (temporal blocking through
+  // the 126 MB L2).
+  int sweep, lag, total;     // total = pairs * per_band work items
+  const int2* order;         // [pairs] (step, band) in execution order (host-built)
   int64_t pitch, plane, origin;
   int64_t nx;                // x extent (interior)
   int64_t row_lo, row_hi;    // valid output rows (2D: y, 3D: z, 1D: unused)
@@ -217,13 +241,30 @@ struct StepParams {
   const uint32_t* e_words;   // [S][128]
 };
 
-constexpr int kEpiWarps = 4;   // one warp per TMEM lane quadrant
-constexpr int kProdWarps = 8;
-constexpr int kMmaWarp = kEpiWarps + kProdWarps;
+// Epilogue: kEpiGroups groups of 4 warps (one warp per TMEM lane quadrant);
+// group g drains the accumulators of the tiles it == g (mod kEpiGroups), so
+// the TMEM -> register -> global path of consecutive tiles overlaps.
+#ifndef SPD_EPI_GROUPS
+#define SPD_EPI_GROUPS 1
+#endif
+#ifndef SPD_PROD_WARPS
+#define SPD_PROD_WARPS 8
+#endif
+constexpr int kEpiGroups = SPD_EPI_GROUPS;
+constexpr int kEpiWarps = 4;                          // warps per epilogue group
+constexpr int kEpiAll = kEpiWarps * kEpiGroups;       // warps 0 .. kEpiAll-1
+constexpr int kProdWarps = SPD_PROD_WARPS;
+constexpr int kMmaWarp = kEpiAll + kProdWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;
-constexpr int kThreads = 32 * (kLoadWarp + 1);
+#ifdef SPD_PUB_WARP
+constexpr int kPubWarp = kLoadWarp + 1;  // persistent launches: publishes finished tiles
+constexpr int kThreads = 32 * (kPubWarp + 1);
+#else
+constexpr int kThreads = 32 * (kLoadWarp + 1);  // publisher = lane 1 of the loader warp
+#endif
+constexpr int kNPub = 4;                 // publish ring depth
 
-template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ>
+template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
 struct Cfg {
   // fast paths: L = 4 (r = 1) and L = 8 (r = 3); any other even L up to 16 uses
   // the generic producer / epilogue
@@ -251,6 +292,9 @@ struct Cfg {
   static constexpr int A_COL = E_COL + 2 * SPD_MAX_S;
   static constexpr int TMEM_COLS = 512;  // host checks A_COL + 8*S <= 512
   static_assert(NTILE % SEG == 0, "tile width must be whole warp segments");
+  // producer work items (input row x warp segment) and items per producer warp
+  static constexpr int N_ITEMS = RIN * SEGS;
+  static constexpr int NQ = (N_ITEMS + kProdWarps - 1) / kProdWarps;
 };
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -294,6 +338,12 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                : "memory");
 }
 
+__device__ __forceinline__ unsigned int ld_relaxed_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -324,10 +374,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 //   loader --(nat_full: tx bytes)--> producers --(nat_empty)--> loader
 //   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
 //   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ, int RIN>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
 __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, NQ>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN>;
   constexpr int KC = C::KC;
+  constexpr int NQ = C::NQ;
   const Geometry& g = p.g;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int sbo = g.b_sbo;
@@ -336,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   uint8_t* nat = smem + NSTAGE * stage_bytes;
   uint8_t* stg = nat + NNAT * p.nat_bytes;  // generic epilogue staging (C::STG_BYTES)
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + C::STG_BYTES);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC + 2 * NNAT);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub);
   const uint32_t bimg_s = smem_u32(bimg);
   const uint32_t nat_s = smem_u32(nat);
   const uint32_t bar_full = smem_u32(bars);
@@ -345,6 +396,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   const uint32_t bar_acce = bar_accf + 8 * NACC;
   const uint32_t bar_natf = bar_acce + 8 * NACC;
   const uint32_t bar_nate = bar_natf + 8 * NNAT;
+  const uint32_t bar_pubf = bar_nate + 8 * NNAT;  // epilogue -> publisher: tile stores issued
+  const uint32_t bar_pube = bar_pubf + 8 * kNPub;  // publisher -> epilogue: slot free
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -362,6 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     for (int a = 0; a < NNAT; ++a) {
       mbar_init(bar_natf + 8 * a, 1);
       mbar_init(bar_nate + 8 * a, kProdWarps);
+    }
+    for (int a = 0; a < kNPub; ++a) {
+      mbar_init(bar_pubf + 8 * a, kEpiWarps);
+      mbar_init(bar_pube + 8 * a, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -402,23 +459,32 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   tc_fence_after();
 
   if (threadIdx.x == 0) SPD_TRACE(14, 0);
-  // Work index g in [0, steps * n_tiles): step t = g / n_tiles, tile in the
-  // step's traversal order (alternating direction: each step starts on the
-  // tiles the previous one wrote last, still resident in L2).  Static
-  // round-robin over CTAs; a tile of step t > 0 first waits (loader) for the
-  // three neighbouring bands of step t-1 — dependencies always point to
-  // smaller g, so with all CTAs co-resident (cooperative launch) the smallest
-  // unfinished tile can always proceed.
-  const int total = p.steps * p.n_tiles;
+  // Work order.  One step (steps == 1): tile t of the step, traversal
+  // direction alternating between launches (each step starts on the tiles the
+  // previous one wrote last, still in L2).  Persistent (steps > 1): the
+  // host-built (step, band) order (sweeps / wavefronts, see StepParams); a
+  // tile of step t > 0 first waits (loader) for the three neighbouring bands
+  // of step t-1 — dependencies point `lag - 1` >= 1 wavefronts back, i.e. to
+  // smaller work indices, so with all CTAs co-resident (cooperative launch)
+  // the smallest unfinished tile can always proceed.  Static round-robin
+  // over CTAs.
+  const int total = p.steps > 1 ? p.total : p.n_tiles;
   struct TileId {
     int step, band;
     int64_t z0, y0, x0;
   };
   auto decode = [&](int gi) {
     TileId id;
-    id.step = gi / p.n_tiles;
-    int t = gi - id.step * p.n_tiles;
-    if ((id.step + p.reverse) & 1) t = p.n_tiles - 1 - t;
+    int t;
+    if (p.steps == 1) {
+      id.step = 0;
+      t = p.reverse ? p.n_tiles - 1 - gi : gi;
+    } else {
+      const int pair = gi / p.per_band;
+      const int2 e = __ldg(p.order + pair);
+      id.step = e.x;
+      t = e.y * p.per_band + (gi - pair * p.per_band);
+    }
     const int bx = t % p.tiles_x;
     const int rest = t / p.tiles_x;
     const int by = rest % p.tiles_y;
@@ -448,12 +514,25 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         if (id.step > 0) {
           // RAW/WAR across steps: the previous step's neighbouring bands are
           // complete (their epilogue stores are visible).
+          // Three independent relaxed polls per round (one L2 round trip,
+          // not three serialised acquires), then one acquire fence.
           const unsigned int need = (unsigned int)(id.step * p.per_band);
           const int b0 = id.band > 0 ? id.band - 1 : 0;
           const int b1 = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
-          for (int b = b0; b <= b1; ++b)
-            while (ld_acquire_gpu(p.band_done + b) < need) __nanosleep(64);
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+          if (p.dbg & 512) {  // debug: full-step barrier semantics
+            for (int b = 0; b < p.n_bands; ++b)
+              while (ld_relaxed_gpu(p.band_done + b) < need) __nanosleep(64);
+          } else if (!(p.dbg & 64)) {
+            while (true) {
+              const unsigned int c0 = ld_relaxed_gpu(p.band_done + b0);
+              const unsigned int c1 = ld_relaxed_gpu(p.band_done + id.band);
+              const unsigned int c2 = ld_relaxed_gpu(p.band_done + b1);
+              if (min(c0, min(c1, c2)) >= need) break;
+              __nanosleep(32);
+            }
+          }
+          if (!(p.dbg & 8192)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          if (!(p.dbg & 4096)) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
         }
         if (p.use_tmap) {
           // select between the two param-space descriptors (a runtime index
@@ -480,14 +559,27 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         SPD_TRACE(1, it);
       }
     }
-  } else if (warp >= kEpiWarps && warp < kMmaWarp) {
+#ifndef SPD_PUB_WARP
+    if (p.steps > 1 && lane == 1) {
+      int it = 0;
+      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+        const TileId id = decode(gi);
+        const int ps = it % kNPub;
+        mbar_wait(bar_pubf + 8 * ps, (it / kNPub) & 1);
+        if (p.dbg & 128) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+        else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+        mbar_arrive(bar_pube + 8 * ps);
+      }
+    }
+#endif
+  } else if (warp >= kEpiAll && warp < kMmaWarp) {
     // ===================== producer: natural rows -> permuted B image =====
     if constexpr (C::GEN) {
       // Generic radius (L = 2r+2 not in {4, 8}): one chunk per lane; the lane
       // reads its 2L-point window as 32-bit words straight from the natural
       // stage and permutes it with compile-time PRMT selectors; window slots
       // past 2L (K-chunk padding) are zero.
-      const int pw = warp - kEpiWarps;
+      const int pw = warp - kEpiAll;
       constexpr int R = (L - 2) / 2;
       constexpr int n_items = RIN * C::SEGS;
       static_assert((NQ - 1) * kProdWarps < n_items && NQ * kProdWarps >= n_items, "NQ must cover the items");
@@ -544,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         }
       }
     } else {
-    const int pw = warp - kEpiWarps;
+    const int pw = warp - kEpiAll;
     constexpr int n_items = RIN * C::SEGS;
     static_assert((NQ - 1) * kProdWarps < n_items && NQ * kProdWarps >= n_items, "NQ must cover the items");
     constexpr int R = (L - 2) / 2;
@@ -654,6 +746,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
+        // (releasing the natural stage right after phase 1 was measured
+        // slower: deeper TMA prefetch only raised load latency)
         mbar_arrive(bar_nate + 8 * ns);
         mbar_arrive(bar_full + 8 * stage);
         if (pw == 0) SPD_TRACE(4, it);
@@ -661,9 +755,31 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       }
     }
     }
+#ifdef SPD_PUB_WARP
+  } else if (warp == kPubWarp) {
+    if (p.steps > 1 && lane == 0) {
+      int it = 0;
+      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+        const TileId id = decode(gi);
+        const int ps = it % kNPub;
+        mbar_wait(bar_pubf + 8 * ps, (it / kNPub) & 1);
+        if (p.dbg & 128) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+        else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+        mbar_arrive(bar_pube + 8 * ps);
+      }
+    }
+#endif
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer ======================================
+    // The whole warp runs the loop (converged, warp-uniform operands in
+    // uniform registers) and one elected lane issues: a divergent lane-0
+    // issue loop costs ~190 cycles per MMA (per-MMA elect loop + R2UR chain)
+    // against ~74 for this form at N = 128 (tools/mma_rate.cu).  The MMA
+    // count and start rows are compile-time (start_row(s) = min(s*RPM,
+    // RIN-RPM), aot.cpp build_geometry).
     const uint32_t idesc = idesc_sparse_f16(128, NTILE, std::is_same<T, __nv_bfloat16>::value);
+    constexpr int RPM = 4 / KC;
+    constexpr int S_CT = (RIN + RPM - 1) / RPM;
     int it = 0;
     for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
@@ -674,25 +790,25 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       if (lane == 0) SPD_TRACE(6, it);
       mbar_wait(bar_full + 8 * stage, sphase);
       tc_fence_after();
-      if (lane == 0) {
-        SPD_TRACE(7, it);
-        const uint32_t sbase = bimg_s + stage * stage_bytes;
-        const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
+      if (lane == 0) SPD_TRACE(7, it);
+      const uint32_t sbase = bimg_s + stage * stage_bytes;
+      const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
+      const uint64_t bdesc0 = umma_desc(sbase, 128, sbo);
 #pragma unroll
-        for (int s = 0; s < SPD_MAX_S; ++s) {
-          if (s < g.s && !(p.dbg & 8)) {
-            const uint64_t bdesc = umma_desc(sbase + g.start_row[s] * KC * 128, 128, sbo);
-            mma_sp_ts(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
-          }
-        }
-        tc_commit(bar_empty + 8 * stage);
-        tc_commit(bar_accf + 8 * acc);
+      for (int s = 0; s < S_CT; ++s) {
+        const int start = s * RPM + RPM <= RIN ? s * RPM : RIN - RPM;
+        // descriptor start address field is addr >> 4
+        const uint64_t bdesc = bdesc0 + (uint64_t)((start * KC * 128) >> 4);
+        mma_sp_ts_elect(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
       }
+      tc_commit_elect(bar_empty + 8 * stage);
+      tc_commit_elect(bar_accf + 8 * acc);
       __syncwarp();
     }
   } else {
     // ===================== epilogue ========================================
     if constexpr (C::GEN) {
+     if (warp < kEpiWarps) {  // one epilogue group (the staging tile is shared)
       // Generic radius: TMEM lane m = L*alpha + i.  Lane pairs (i, i+1) pack
       // their fp16 values through a shuffle, store 32-bit words into a staging
       // tile [alpha][32*L points] (pitch 66L bytes: consecutive lanes hit
@@ -779,15 +895,19 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           if (cb + 1 < NB) tmem_wait_ld();
         }
         if (p.steps > 1) {
-          asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-          if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(p.band_done + id.band, 1u);
-          }
+          // hand the tile to the publisher warp (release at CTA scope after
+          // the warp's stores); the gpu-scope release happens off this path
+          const int ps = it % kNPub;
+          mbar_wait(bar_pube + 8 * ps, ((it / kNPub) & 1) ^ 1);
+          if (p.dbg & 256) __threadfence();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
         }
       }
+     }
     } else {
-    const int quad = warp;  // TMEM lane quadrant
+    const int quad = warp % 4;       // TMEM lane quadrant (warp id mod 4)
+    const int grp = warp / 4;        // epilogue group: tiles it == grp (mod kEpiGroups)
     const int m = quad * 32 + lane;  // TMEM lane == M row
     const int alpha = m / L;         // output row of the tile
     const int d = lane % L;          // position in the L-lane group
@@ -795,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
     int it = 0;
     for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+      if (kEpiGroups > 1 && (it % kEpiGroups) != grp) continue;
       const int acc = it % NACC;
       const uint32_t aphase = (it / NACC) & 1;
       const TileId id = decode(gi);
@@ -895,12 +1016,13 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       }
       if (warp == 0 && lane == 0) SPD_TRACE(9, it);
       if (p.steps > 1) {
-        // publish: this tile's stores are complete (epilogue warps only)
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (threadIdx.x == 0) {
-          __threadfence();
-          atomicAdd(p.band_done + id.band, 1u);
-        }
+        // hand the tile to the publisher warp (release at CTA scope after
+        // the warp's stores); the gpu-scope release happens off this path
+        const int ps = it % kNPub;
+        mbar_wait(bar_pube + 8 * ps, ((it / kNPub) & 1) ^ 1);
+        if (p.dbg & 256) __threadfence();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
       }
     }
     }
@@ -1093,6 +1215,8 @@ struct spd_plan {
   unsigned int* d_counters = nullptr;  // per-band completion counters (persistent runs)
   int counters_cap = 0;
   int sms = 0;
+  // persistent work orders (device), keyed by (steps, sweep, lag, n_bands)
+  std::map<std::tuple<int, int, int, int>, int2*> orders;
 };
 
 namespace spd {
@@ -1112,11 +1236,18 @@ static int plan_counters(const spd_plan* cplan, int n, cudaStream_t st, unsigned
   return cuda_err(cudaMemsetAsync(plan->d_counters, 0, sizeof(unsigned int) * n, st), "counter reset");
 }
 
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int NQ, int RIN>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, NQ>;
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, NQ, RIN>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN>;
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
+  {  // the MMA issuer's compile-time schedule must be the plan's
+    constexpr int RPM = 4 / C::KC;
+    if (plan->g.s != (RIN + RPM - 1) / RPM) return set_error(SPD_EUNSUPPORTED, "MMA count mismatch (%d)", plan->g.s);
+    for (int s = 0; s < plan->g.s; ++s)
+      if (plan->g.start_row[s] != (s * RPM + RPM <= RIN ? s * RPM : RIN - RPM))
+        return set_error(SPD_EUNSUPPORTED, "MMA start row mismatch (%d)", s);
+  }
   sp.nat_bytes = sp.use_tmap ? sp.nbox * sp.box_slot : plan->g.r_in * C::ROW_BYTES;
   if (!sp.use_tmap) {
     sp.nbox = 1;
@@ -1124,7 +1255,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     sp.box_slot = sp.nat_bytes;
   }
   const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + (size_t)NNAT * sp.nat_bytes + C::STG_BYTES +
-                      8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT) + 16;
+                      8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub) + 16;
   if (smem > 232448) return set_error(SPD_EUNSUPPORTED, "shared memory budget exceeded (%zu B)", smem);
   if (C::A_COL + 8 * plan->g.s > 512) return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
   static thread_local int configured_dev = -1;
@@ -1157,22 +1288,22 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   // <T, L, PARITY, NTILE, B-image stages, natural-row stages, accumulator
   //  stages, items per producer warp>; stage counts fill the 227 KB of smem
   // (scan in profiles/r01_tuning.txt).
-  if (g.L == 4 && g.n_tile == 128 && g.r_in == 34) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 9, 34>(plan, sp, st);
-  if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 8, 32>(plan, sp, st);
-  if (g.L == 4 && g.n_tile == 64 && g.r_in == 60) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 8, 60>(plan, sp, st);
-  if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 6, 22>(plan, sp, st);
-  if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 4, 16>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 128 && g.r_in == 34) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 34>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 64 && g.r_in == 60) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 60>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 22>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16>(plan, sp, st);
   // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
-  if (g.L == 6 && g.r_in == 25) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 7, 25>(plan, sp, st);
-  if (g.L == 6 && g.r_in == 21) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 6, 21>(plan, sp, st);
-  if (g.L == 10 && g.r_in == 20) return launch_step<T, 10, PARITY, 64, 2, 1, 4, 5, 20>(plan, sp, st);
-  if (g.L == 10 && g.r_in == 12) return launch_step<T, 10, PARITY, 64, 2, 2, 4, 3, 12>(plan, sp, st);
-  if (g.L == 12 && g.r_in == 20) return launch_step<T, 12, PARITY, 64, 2, 1, 4, 5, 20>(plan, sp, st);
-  if (g.L == 12 && g.r_in == 10) return launch_step<T, 12, PARITY, 64, 2, 2, 4, 3, 10>(plan, sp, st);
-  if (g.L == 14 && g.r_in == 21) return launch_step<T, 14, PARITY, 64, 2, 1, 4, 6, 21>(plan, sp, st);
-  if (g.L == 14 && g.r_in == 9) return launch_step<T, 14, PARITY, 64, 2, 2, 4, 3, 9>(plan, sp, st);
-  if (g.L == 16 && g.r_in == 22) return launch_step<T, 16, PARITY, 64, 1, 1, 4, 6, 22>(plan, sp, st);
-  if (g.L == 16 && g.r_in == 8) return launch_step<T, 16, PARITY, 64, 2, 2, 4, 2, 8>(plan, sp, st);
+  if (g.L == 6 && g.r_in == 25) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 25>(plan, sp, st);
+  if (g.L == 6 && g.r_in == 21) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 21>(plan, sp, st);
+  if (g.L == 10 && g.r_in == 20) return launch_step<T, 10, PARITY, 64, 2, 1, 4, 20>(plan, sp, st);
+  if (g.L == 10 && g.r_in == 12) return launch_step<T, 10, PARITY, 64, 2, 2, 4, 12>(plan, sp, st);
+  if (g.L == 12 && g.r_in == 20) return launch_step<T, 12, PARITY, 64, 2, 1, 4, 20>(plan, sp, st);
+  if (g.L == 12 && g.r_in == 10) return launch_step<T, 12, PARITY, 64, 2, 2, 4, 10>(plan, sp, st);
+  if (g.L == 14 && g.r_in == 21) return launch_step<T, 14, PARITY, 64, 2, 1, 4, 21>(plan, sp, st);
+  if (g.L == 14 && g.r_in == 9) return launch_step<T, 14, PARITY, 64, 2, 2, 4, 9>(plan, sp, st);
+  if (g.L == 16 && g.r_in == 22) return launch_step<T, 16, PARITY, 64, 1, 1, 4, 22>(plan, sp, st);
+  if (g.L == 16 && g.r_in == 8) return launch_step<T, 16, PARITY, 64, 2, 2, 4, 8>(plan, sp, st);
   return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
 }
 
@@ -1285,7 +1416,7 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     sp.n_bands = sp.tiles_x;
     sp.per_band = 1;
   }
-  static const char* dbg_env = getenv("SPD_DBG");
+  const char* dbg_env = getenv("SPD_DBG");
   sp.dbg = dbg_env ? atoi(dbg_env) : 0;
   static const char* pf_env = getenv("SPD_PREFETCH");
   sp.prefetch = pf_env ? atoi(pf_env) : 0;
@@ -1307,6 +1438,57 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     if (rc) return rc;
     return make_tensor_map(plan, gd, buf1, sp, &sp.tmap[1]);
   }
+  return SPD_OK;
+}
+
+// Persistent work order: sweeps of S steps, step s+1 lagging step s by `lag`
+// bands.  The data step s writes is re-read by step s+1 about `lag`
+// wavefronts later; S is sized so that everything in flight between the
+// leading and trailing steps of a sweep (~ 2 buffers x lag x S bands) stays
+// well inside the 126 MB L2.  SPD_SWEEP / SPD_LAG override (tuning).
+static int wavefront_order(const spd_plan* cplan, const spd_grid_desc* gd, StepParams& sp) {
+  spd_plan* plan = const_cast<spd_plan*>(cplan);
+  const Geometry& g = plan->g;
+  const int64_t band_bytes =
+      2 * (g.d == 3 ? (int64_t)g.tile_z * gd->plane : (g.d == 2 ? (int64_t)g.tile_y * gd->pitch : (int64_t)g.tile_x));
+  const char* lag_env = getenv("SPD_LAG");
+  const char* sweep_env = getenv("SPD_SWEEP");
+  int lag = lag_env ? atoi(lag_env) : 3;
+  if (lag < 2) lag = 2;
+  int64_t S = (int64_t)40 << 20;
+  S /= 2 * lag * (band_bytes > 0 ? band_bytes : 1);
+  if (sweep_env) S = atoi(sweep_env);
+  if (S < 1) S = 1;
+  if (S > 64) S = 64;
+  if (S > sp.steps) S = sp.steps;
+  sp.sweep = (int)S;
+  sp.lag = lag;
+  const int64_t pairs = (int64_t)sp.steps * sp.n_bands;
+  if (pairs * sp.per_band >= ((int64_t)1 << 31))
+    return set_error(SPD_EINVAL, "persistent launch too large (%lld work items)", (long long)(pairs * sp.per_band));
+  sp.total = (int)(pairs * sp.per_band);
+  const auto key = std::make_tuple(sp.steps, sp.sweep, sp.lag, sp.n_bands);
+  auto it = plan->orders.find(key);
+  if (it == plan->orders.end()) {
+    // built once per key (synchronous upload: warm up outside graph capture)
+    std::vector<int2> order;
+    order.reserve((size_t)pairs);
+    for (int k0 = 0; k0 < sp.steps; k0 += sp.sweep) {
+      const int sk = sp.steps - k0 < sp.sweep ? sp.steps - k0 : sp.sweep;
+      for (int w = 0; w < lag * (sk - 1) + sp.n_bands; ++w)
+        for (int s = 0; s < sk; ++s) {
+          const int band = w - lag * s;
+          if (band >= 0 && band < sp.n_bands) order.push_back(make_int2(k0 + s, band));
+        }
+    }
+    int2* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(int2) * order.size());
+    if (e != cudaSuccess) return cuda_err(e, "order alloc");
+    e = cudaMemcpy(d, order.data(), sizeof(int2) * order.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_err(e, "order upload");
+    it = plan->orders.emplace(key, d).first;
+  }
+  sp.order = it->second;
   return SPD_OK;
 }
 
@@ -1393,6 +1575,7 @@ int spd_plan_destroy(spd_plan* plan) {
   if (plan->d_a) cudaFree(plan->d_a);
   if (plan->d_e) cudaFree(plan->d_e);
   if (plan->d_counters) cudaFree(plan->d_counters);
+  for (auto& kv : plan->orders) cudaFree(kv.second);
   delete plan;
   return SPD_OK;
 }
@@ -1508,19 +1691,26 @@ int spd_run_ex(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* 
   if (rc) return rc;
   if (steps < 1) return set_error(SPD_EINVAL, "step count must be >= 1, got %d", steps);
   // Default: one launch per step (alternating traversal for L2 reuse).
-  // SPD_RUN_PERSISTENT: one cooperative launch for all steps, ordered by
-  // per-band completion counters (correct, currently slower: the per-tile
-  // publish fence costs more than the launch boundaries it removes; see
-  // DESIGN.md §7).
+  // SPD_RUN_PERSISTENT: one cooperative launch for all steps, in sweep /
+  // wavefront order (temporal blocking through L2), ordered by per-band
+  // completion counters; bit-identical to the per-step launches.
   const bool persistent = (flags & SPD_RUN_PERSISTENT) != 0;
   const int64_t extent = plan->d == 3 ? gd->nz : (plan->d == 2 ? gd->ny : 1);
   int done = 0;
   while (done < steps) {
-    const int chunk = persistent ? (steps - done > 100000 ? 100000 : steps - done) : 1;
+    int chunk = persistent ? steps - done : 1;
     StepParams sp;
     rc = fill_step_params(plan, gd, done % 2 ? buf1 : buf0, done % 2 ? buf0 : buf1, 0, extent, chunk, sp);
     if (rc) return rc;
     if (chunk > 1) {
+      // keep the work count in int range
+      const int64_t cap = ((int64_t)1 << 30) / ((int64_t)sp.n_bands * sp.per_band);
+      if (chunk > cap) {
+        chunk = (int)cap;
+        sp.steps = chunk;
+      }
+      rc = wavefront_order(plan, gd, sp);
+      if (rc) return rc;
       rc = plan_counters(plan, sp.n_bands, (cudaStream_t)stream, &sp.band_done);
       if (rc) return rc;
     }

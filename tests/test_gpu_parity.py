@@ -317,17 +317,41 @@ def test_slab_driver_emulated_ranks_bit_exact(d, shape, ranks):
         assert torch.equal(got[h:-h], want[h + s.lo : h + s.hi]), (s.lo, s.hi)
 
 
-@pytest.mark.parametrize("d,shape", [(2, (512, 512)), (2, (100, 1000)), (3, (16, 24, 128)), (1, (1, 40000))])
-def test_persistent_launch_matches_per_step(d, shape):
-    """One cooperative launch for all steps (band-counter ordered) gives the
-    same bits as one launch per step."""
-    k = rand_kernel("box", d, 1, seed=[d, 31])
+@pytest.mark.parametrize(
+    "d,r,shape,steps,sweep,lag",
+    [
+        (2, 1, (512, 512), 6, None, None),
+        (2, 1, (100, 1000), 6, None, None),
+        (3, 1, (16, 24, 128), 6, None, None),
+        (1, 1, (1, 40000), 6, None, None),
+        (2, 1, (1000, 2048), 13, 1, 2),
+        (2, 1, (1000, 2048), 13, 4, 2),
+        (2, 1, (1000, 2048), 13, 5, 3),
+        (2, 1, (1000, 2048), 13, 13, 4),
+        (2, 3, (600, 1024), 9, 4, 2),
+        (2, 2, (300, 1536), 7, 3, 2),
+        (3, 1, (64, 40, 256), 11, 3, 2),
+        (1, 1, (1, 100000), 9, 4, 2),
+    ],
+)
+def test_persistent_launch_matches_per_step(monkeypatch, d, r, shape, steps, sweep, lag):
+    """One cooperative launch for all steps (sweep / wavefront order through
+    L2, band-counter ordered) gives the same bits as one launch per step, for
+    every sweep length and band lag (partial last sweeps included)."""
+    if sweep is not None:
+        monkeypatch.setenv("SPD_SWEEP", str(sweep))
+        monkeypatch.setenv("SPD_LAG", str(lag))
+    # normalised weights: many steps of un-normalised r = 3 weights overflow
+    # fp16 to inf/NaN, and NaN != NaN
+    k0 = rand_kernel("box", d, r, seed=[d, 31 + r])
+    c = k0.coeffs / np.abs(k0.coeffs).sum()
+    k = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
     plan = get_plan(k, sp.Parity.EVEN, "fp16")
-    dense = torch.rand(tuple(n + 2 for n in shape), dtype=torch.float64, device="cuda") - 0.5
+    dense = torch.rand(tuple(n + 2 * r for n in shape), dtype=torch.float64, device="cuda") - 0.5
     outs = []
     for persistent in (False, True):
-        g = DeviceGrid(plan, shape, 1)
+        g = DeviceGrid(plan, shape, r)
         g.load_dense_f64(dense)
-        g.run(6, persistent=persistent)
+        g.run(steps, persistent=persistent)
         outs.append(g.bufs[g.cur].clone())
     assert torch.equal(outs[0], outs[1])
