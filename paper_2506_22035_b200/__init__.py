@@ -41,6 +41,8 @@ from .transform import (
     swap_columns,
 )
 
+from .io import load_grid, load_kernel, save_grid, save_kernel
+
 __version__ = "0.1.0"
 
 
@@ -62,6 +64,10 @@ def __getattr__(name):
 
 
 __all__ = [
+    "load_grid",
+    "load_kernel",
+    "save_grid",
+    "save_kernel",
     "Grid",
     "Grid3D",
     "Shape",

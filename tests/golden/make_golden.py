@@ -177,8 +177,33 @@ def naive3d_cases(ss):
     print("naive3d_golden.npz: rho_z=0 and separable pins")
 
 
+def io_cases(ss):
+    """Reference-written files for the byte-compatibility tests of io.py."""
+    from sparsestencil import transform as st
+
+    d = OUT / "io"
+    d.mkdir(exist_ok=True)
+    ss.save_grid(ss.random_grid(5, 7, 2, seed=3), d / "grid.spgr")
+    rng = np.random.default_rng(7)
+    k = ss.make_kernel("box", 2, 3, rng.uniform(-1, 1, (7, 7)))
+    ss.save_kernel(k, d / "box2d_r3.json")
+    star = np.zeros((3, 3))
+    star[1, :] = [0.25, -0.5, 0.25]
+    star[:, 1] = [0.125, -0.5, 0.125]
+    ss.save_kernel(ss.make_kernel("star", 2, 1, star), d / "star2d_r1.json")
+    for name in ("box2d_r3", "star2d_r1"):
+        kern = ss.load_kernel(d / f"{name}.json")
+        for par in ("even", "odd"):
+            ts = ss.transform_stencil(kern, ss.Parity(par))
+            cks = [ck for _rho, ck in ts.rows]
+            st.save_compressed_set(cks, d / f"{name}_{par}.spck")
+            st.save_compressed_json(cks, d / f"{name}_{par}.spck.json")
+    print("io/: SPGR grid, kernel JSON, SPCK records + JSON mirrors")
+
+
 if __name__ == "__main__":
     ss = _ref()
     transform_cases(ss)
     naive_cases(ss)
     naive3d_cases(ss)
+    io_cases(ss)

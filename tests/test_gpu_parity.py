@@ -393,3 +393,32 @@ def test_many_tiles_per_cta_match_oracle(d, r, shape, steps, persistent):
     assert max_rel_error(got, want) < TOL["fp16"]
     # fp32 accumulation + one fp16 rounding per step: far tighter than 1e-2
     assert np.abs(got - want).max() < 2e-3 * np.abs(want).max()
+
+
+def test_cli_run_and_verify_on_device(tmp_path, capsys):
+    """The reference CLI surface (cli.py:74-97, 185-203) over the device:
+    make-grid -> run -> SPGR output vs the oracle; verify exits 0."""
+    import json
+    from pathlib import Path
+
+    from paper_2506_22035_b200 import cli
+    from paper_2506_22035_b200.io import load_grid, load_kernel
+
+    gold = Path(__file__).resolve().parent / "golden" / "io"
+    assert cli.main(["make-grid", "--size", "96x256", "--halo", "1", "--seed", "5",
+                     "--out", str(tmp_path / "g.spgr")]) == cli.EXIT_OK
+    capsys.readouterr()
+    assert cli.main(["run", "--kernel", str(gold / "star2d_r1.json"), "--grid", str(tmp_path / "g.spgr"),
+                     "--steps", "3", "--out", str(tmp_path / "o.spgr"), "--stats"]) == cli.EXIT_OK
+    payload = json.loads(capsys.readouterr().out)
+    assert payload["stats"]["steps"] == 3 and payload["stats"]["kernel_rows"] == 3
+    k = load_kernel(gold / "star2d_r1.json")
+    g = load_grid(tmp_path / "g.spgr")
+    q = quant(g.data)
+    want = cnaive.naive_apply(k.coeffs, 2, 1, q, 1, 3)
+    got = load_grid(tmp_path / "o.spgr")
+    assert max_rel_error(got.interior, want[1:-1, 1:-1]) < TOL["fp16"]
+    assert abs(payload["output_checksum"] - float(got.interior.sum())) < 1e-6 * max(1.0, abs(payload["output_checksum"]))
+    assert cli.main(["verify", "--kernel", str(gold / "box2d_r3.json"), "--sizes", "48,80", "--steps", "1"]) == cli.EXIT_OK
+    out = capsys.readouterr().out
+    assert "all_pass:" in out
