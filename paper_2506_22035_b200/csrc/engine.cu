@@ -69,6 +69,17 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking phase test.
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred P1;\nmbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -256,13 +267,15 @@ constexpr int kEpiAll = kEpiWarps * kEpiGroups;       // warps 0 .. kEpiAll-1
 constexpr int kProdWarps = SPD_PROD_WARPS;
 constexpr int kMmaWarp = kEpiAll + kProdWarps;
 constexpr int kLoadWarp = kMmaWarp + 1;
-#ifdef SPD_PUB_WARP
-constexpr int kPubWarp = kLoadWarp + 1;  // persistent launches: publishes finished tiles
-constexpr int kThreads = 32 * (kPubWarp + 1);
-#else
-constexpr int kThreads = 32 * (kLoadWarp + 1);  // publisher = lane 1 of the loader warp
-#endif
-constexpr int kNPub = 4;                 // publish ring depth
+// Persistent launches only (idle in one-step launches): the publisher makes
+// finished tiles visible and bumps band counters; the poller runs up to kDQ
+// tiles ahead of the loader, waiting for each tile's dependencies (so the
+// loader never holds an L2 round trip + gpu-scope fence on its path).
+constexpr int kPubWarp = kLoadWarp + 1;
+constexpr int kPollWarp = kPubWarp + 1;
+constexpr int kThreads = 32 * (kPollWarp + 1);
+constexpr int kDQ = 8;                   // poller -> loader ring depth
+constexpr int kNPub = 8;                 // publish ring depth (max tiles per publish batch)
 
 template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
 struct Cfg {
@@ -387,7 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   uint8_t* nat = smem + NSTAGE * stage_bytes;
   uint8_t* stg = nat + NNAT * p.nat_bytes;  // generic epilogue staging (C::STG_BYTES)
   uint64_t* bars = reinterpret_cast<uint64_t*>(stg + C::STG_BYTES);
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub + 2 * kDQ);
   const uint32_t bimg_s = smem_u32(bimg);
   const uint32_t nat_s = smem_u32(nat);
   const uint32_t bar_full = smem_u32(bars);
@@ -398,6 +411,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   const uint32_t bar_nate = bar_natf + 8 * NNAT;
   const uint32_t bar_pubf = bar_nate + 8 * NNAT;  // epilogue -> publisher: tile stores issued
   const uint32_t bar_pube = bar_pubf + 8 * kNPub;  // publisher -> epilogue: slot free
+  const uint32_t bar_depf = bar_pube + 8 * kNPub;   // poller -> loader: tile's inputs are final
+  const uint32_t bar_depe = bar_depf + 8 * kDQ;     // loader -> poller: slot free
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -419,6 +434,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     for (int a = 0; a < kNPub; ++a) {
       mbar_init(bar_pubf + 8 * a, kEpiWarps);
       mbar_init(bar_pube + 8 * a, 1);
+    }
+    for (int a = 0; a < kDQ; ++a) {
+      mbar_init(bar_depf + 8 * a, 1);
+      mbar_init(bar_depe + 8 * a, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -473,17 +492,22 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     int step, band;
     int64_t z0, y0, x0;
   };
-  auto decode = [&](int gi) {
+  // Persistent order entries are fetched one tile ahead (the fetch for the
+  // next tile is issued before this tile's work), so the dependent global
+  // load never sits on a role's critical path.
+  auto fetch = [&](int gi) -> int2 {
+    if (p.steps == 1 || gi >= total) return make_int2(0, 0);
+    return __ldg(p.order + gi / p.per_band);
+  };
+  auto decode_e = [&](int gi, int2 e) {
     TileId id;
     int t;
     if (p.steps == 1) {
       id.step = 0;
       t = p.reverse ? p.n_tiles - 1 - gi : gi;
     } else {
-      const int pair = gi / p.per_band;
-      const int2 e = __ldg(p.order + pair);
       id.step = e.x;
-      t = e.y * p.per_band + (gi - pair * p.per_band);
+      t = e.y * p.per_band + gi % p.per_band;
     }
     const int bx = t % p.tiles_x;
     const int rest = t / p.tiles_x;
@@ -496,6 +520,31 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     return id;
   };
 
+
+  // Publisher (persistent launches): after all epilogue warps issued a
+  // tile's stores (pubf), make them visible at gpu scope and bump the tile's
+  // band counter.  Tiles whose stores are already issued are batched behind
+  // ONE fence.acq_rel.gpu (cumulative over the epilogue's stores through the
+  // CTA-scope mbarrier release/acquire) followed by relaxed increments: the
+  // fence waits for the store drain, so one fence per tile cannot keep up
+  // with short tiles.
+  auto publisher = [&]() {
+    int it = 0;
+    for (int gi = blockIdx.x; gi < total;) {
+      mbar_wait(bar_pubf + 8 * (it % kNPub), (it / kNPub) & 1);
+      int n = 1;
+      while (n < kNPub && gi + n * (int)gridDim.x < total &&
+             mbar_test(bar_pubf + 8 * ((it + n) % kNPub), ((it + n) / kNPub) & 1))
+        ++n;
+      if (!(p.dbg & 128)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (int j = 0; j < n; ++j, ++it, gi += gridDim.x) {
+        const TileId id = decode_e(gi, fetch(gi));
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+        mbar_arrive(bar_pube + 8 * (it % kNPub));
+      }
+    }
+  };
+
   if (warp == kLoadWarp) {
     // ===================== loader: TMA copies of the natural input rows ===
     // 2D/3D: the tile's halo-padded input block as nbox tensor boxes
@@ -503,35 +552,24 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     if (lane == 0) {
       const uint32_t box_bytes = (uint32_t)(p.boxw * 2 * g.r_in);
       int it = 0;
+      int2 e_nx = fetch(blockIdx.x);
+      int e_gi = blockIdx.x;
       for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
         const int ns = it % NNAT;
         const uint32_t nphase = (it / NNAT) & 1;
-        const TileId id = decode(gi);
+        const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
+        e_nx = fetch(gi + gridDim.x);
+        e_gi = gi + gridDim.x;
+        const TileId id = decode_e(gi, e_cur);
         const uint32_t dst = nat_s + ns * p.nat_bytes;
         const uint32_t fb = bar_natf + 8 * ns;
         SPD_TRACE(0, it);
         mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
-        if (id.step > 0) {
-          // RAW/WAR across steps: the previous step's neighbouring bands are
-          // complete (their epilogue stores are visible).
-          // Three independent relaxed polls per round (one L2 round trip,
-          // not three serialised acquires), then one acquire fence.
-          const unsigned int need = (unsigned int)(id.step * p.per_band);
-          const int b0 = id.band > 0 ? id.band - 1 : 0;
-          const int b1 = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
-          if (p.dbg & 512) {  // debug: full-step barrier semantics
-            for (int b = 0; b < p.n_bands; ++b)
-              while (ld_relaxed_gpu(p.band_done + b) < need) __nanosleep(64);
-          } else if (!(p.dbg & 64)) {
-            while (true) {
-              const unsigned int c0 = ld_relaxed_gpu(p.band_done + b0);
-              const unsigned int c1 = ld_relaxed_gpu(p.band_done + id.band);
-              const unsigned int c2 = ld_relaxed_gpu(p.band_done + b1);
-              if (min(c0, min(c1, c2)) >= need) break;
-              __nanosleep(32);
-            }
-          }
-          if (!(p.dbg & 8192)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (p.steps > 1) {
+          // RAW/WAR across steps: the poller has seen the previous step's
+          // neighbouring bands complete (gpu-scope acquire) and released this
+          // slot; the CTA-scope acquire here extends that to the TMA reads.
+          mbar_wait(bar_depf + 8 * (it % kDQ), (it / kDQ) & 1);
           if (!(p.dbg & 4096)) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
         }
         if (p.use_tmap) {
@@ -556,22 +594,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             bulk_g2s(dst + b * C::ROW_BYTES, src, C::ROW_BYTES, fb);
           }
         }
+        if (p.steps > 1) mbar_arrive(bar_depe + 8 * (it % kDQ));
         SPD_TRACE(1, it);
       }
     }
-#ifndef SPD_PUB_WARP
-    if (p.steps > 1 && lane == 1) {
-      int it = 0;
-      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
-        const TileId id = decode(gi);
-        const int ps = it % kNPub;
-        mbar_wait(bar_pubf + 8 * ps, (it / kNPub) & 1);
-        if (p.dbg & 128) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
-        else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
-        mbar_arrive(bar_pube + 8 * ps);
-      }
-    }
-#endif
   } else if (warp >= kEpiAll && warp < kMmaWarp) {
     // ===================== producer: natural rows -> permuted B image =====
     if constexpr (C::GEN) {
@@ -755,20 +781,53 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       }
     }
     }
-#ifdef SPD_PUB_WARP
   } else if (warp == kPubWarp) {
+    if (p.steps > 1 && lane == 0) publisher();
+  } else if (warp == kPollWarp) {
+    // ===================== dependency poller (persistent launches) =========
+    // Tiles whose dependencies are already met are released in batches of
+    // up to kDQ/2 behind ONE acquire fence (a gpu-scope fence per tile cannot
+    // keep up with 3D tiles).  A tile that must wait first flushes the batch:
+    // its dependencies may be tiles of this very batch.
     if (p.steps > 1 && lane == 0) {
+      constexpr int kBatch = kDQ / 2;
+      int pending = 0;        // gathered, not yet released (tiles it-pending .. it-1)
+      bool pend_dep = false;  // some pending tile has dependencies (needs the fence)
+      auto flush = [&](int it_end) {
+        if (pending == 0) return;
+        if (pend_dep && !(p.dbg & 8192)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int t = it_end - pending; t < it_end; ++t) mbar_arrive(bar_depf + 8 * (t % kDQ));
+        pending = 0;
+        pend_dep = false;
+      };
       int it = 0;
       for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
-        const TileId id = decode(gi);
-        const int ps = it % kNPub;
-        mbar_wait(bar_pubf + 8 * ps, (it / kNPub) & 1);
-        if (p.dbg & 128) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
-        else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
-        mbar_arrive(bar_pube + 8 * ps);
+        const TileId id = decode_e(gi, fetch(gi));
+        mbar_wait(bar_depe + 8 * (it % kDQ), ((it / kDQ) & 1) ^ 1);
+        if (id.step > 0) {
+          // a tile of step t reads the three neighbouring bands of step t-1
+          // (RAW) and overwrites what step t-1 read (WAR): relaxed polls of
+          // the three band counters
+          const unsigned int need = (unsigned int)(id.step * p.per_band);
+          const int b0 = id.band > 0 ? id.band - 1 : 0;
+          const int b1 = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
+          bool first = true;
+          while (!(p.dbg & 64)) {
+            const unsigned int c0 = ld_relaxed_gpu(p.band_done + b0);
+            const unsigned int c1 = ld_relaxed_gpu(p.band_done + id.band);
+            const unsigned int c2 = ld_relaxed_gpu(p.band_done + b1);
+            if (min(c0, min(c1, c2)) >= need) break;
+            if (first) flush(it);
+            first = false;
+            __nanosleep(32);
+          }
+          pend_dep = true;
+        }
+        ++pending;
+        if (pending == kBatch) flush(it + 1);
       }
+      flush(it);
     }
-#endif
   } else if (warp == kMmaWarp) {
     // ===================== MMA issuer ======================================
     // The whole warp runs the loop (converged, warp-uniform operands in
@@ -834,10 +893,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
       int bt = 0;
       int it = 0;
+      int2 e_nx = fetch(blockIdx.x);
+      int e_gi = blockIdx.x;
       for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
         const int acc = it % NACC;
         const uint32_t aphase = (it / NACC) & 1;
-        const TileId id = decode(gi);
+        const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
+        e_nx = fetch(gi + gridDim.x);
+        e_gi = gi + gridDim.x;
+        const TileId id = decode_e(gi, e_cur);
         T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
         mbar_wait(bar_accf + 8 * acc, aphase);
         tc_fence_after();
@@ -914,11 +978,16 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
     int it = 0;
+    int2 e_nx = fetch(blockIdx.x);
+    int e_gi = blockIdx.x;
     for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       if (kEpiGroups > 1 && (it % kEpiGroups) != grp) continue;
       const int acc = it % NACC;
       const uint32_t aphase = (it / NACC) & 1;
-      const TileId id = decode(gi);
+      const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
+      e_nx = fetch(gi + gridDim.x);
+      e_gi = gi + gridDim.x;
+      const TileId id = decode_e(gi, e_cur);
       T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
       const int64_t z = id.z0 + odz;
       const int64_t y = id.y0 + ody;
@@ -1255,7 +1324,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     sp.box_slot = sp.nat_bytes;
   }
   const size_t smem = (size_t)NSTAGE * (NTILE / 8) * plan->g.b_sbo + (size_t)NNAT * sp.nat_bytes + C::STG_BYTES +
-                      8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub) + 16;
+                      8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub + 2 * kDQ) + 16;
   if (smem > 232448) return set_error(SPD_EUNSUPPORTED, "shared memory budget exceeded (%zu B)", smem);
   if (C::A_COL + 8 * plan->g.s > 512) return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
   static thread_local int configured_dev = -1;

@@ -334,6 +334,7 @@ def test_slab_driver_emulated_ranks_bit_exact(d, shape, ranks):
         (1, 1, (1, 100000), 9, 4, 2),
     ],
 )
+@pytest.mark.timeout(180, method="thread")
 def test_persistent_launch_matches_per_step(monkeypatch, d, r, shape, steps, sweep, lag):
     """One cooperative launch for all steps (sweep / wavefront order through
     L2, band-counter ordered) gives the same bits as one launch per step, for
@@ -376,6 +377,7 @@ def test_persistent_launch_matches_per_step(monkeypatch, d, r, shape, steps, swe
     ],
 )
 @pytest.mark.parametrize("persistent", [False, True])
+@pytest.mark.timeout(180, method="thread")
 def test_many_tiles_per_cta_match_oracle(d, r, shape, steps, persistent):
     import os
 
