@@ -266,19 +266,26 @@ def run_ours(args, cfg_name):
         grid.load_dense_f64(dense)
         del dense
         launches_per_step = T
-        graph = torch.cuda.CUDAGraph()
-        # capture T steps (an even T keeps the buffer parity fixed per replay)
-        s = torch.cuda.Stream()
-        s.wait_stream(stream)
-        with torch.cuda.stream(s):
-            grid.run(T)  # warm the kernel attributes outside capture
-        stream.wait_stream(s)
-        torch.cuda.synchronize()
-        with torch.cuda.graph(graph):
-            grid.run(T)
+        if args.graph:
+            graph = torch.cuda.CUDAGraph()
+            # capture T steps (an even T keeps the buffer parity fixed per replay)
+            s = torch.cuda.Stream()
+            s.wait_stream(stream)
+            with torch.cuda.stream(s):
+                grid.run(T)  # warm the kernel attributes outside capture
+            stream.wait_stream(s)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph):
+                grid.run(T)
 
-        def one_step():
-            graph.replay()
+            def one_step():
+                graph.replay()
+        else:
+            # T step kernels straight into the stream: consecutive launches
+            # overlap through programmatic dependent launch (measured faster
+            # than a CUDA-graph replay of the same T launches)
+            def one_step():
+                grid.run(T)
     else:
         from paper_2506_22035_b200.distributed import DeviceSlabOps, Slab, SlabDriver
 
@@ -384,6 +391,7 @@ def run_ours(args, cfg_name):
             "data": "synthetic U(-1,1) grid, contractive normalised weights (random init)",
             "config": {"workload": cfg_name, "description": desc, "grid_per_gpu": list(shape),
                        "timesteps_per_step": T, "parallelism": f"slab{world}" if slab_mode else "single",
+                       "launch": "cuda-graph" if args.graph else "stream, programmatic dependent launch",
                        "l2": f"inputs larger than L2 ({2 * np.prod(dense_shape) / 2**20:.0f} MiB per buffer)",
                        "tile": {"L": info.L, "n_tile": info.n_tile, "mmas_per_tile": info.mmas_per_tile},
                        "slab": slab},
@@ -409,6 +417,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true", help="use the multi-GPU slab driver even at N=1")
+    ap.add_argument("--graph", action="store_true", help="replay the T step launches as one CUDA graph")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

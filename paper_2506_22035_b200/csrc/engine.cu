@@ -417,6 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (threadIdx.x == 0) SPD_TRACE(13, 0);
+  // let the next step kernel in the stream start its prologue as soon as
+  // SMs free up (it still waits for this grid in griddepcontrol.wait)
+  if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
@@ -476,6 +479,11 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, resident A/E operands) overlaps the previous step kernel's
+  // tail; the grids it reads and writes are touched only after the previous
+  // grid has completed and its writes are visible.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (threadIdx.x == 0) SPD_TRACE(14, 0);
   // Work order.  One step (steps == 1): tile t of the step, traversal
@@ -1344,8 +1352,14 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: cross-step waits need every CTA running
-  attr[0].val.cooperative = sp.steps > 1 ? 1 : 0;
+  if (sp.steps > 1) {
+    attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: cross-step waits need every CTA running
+    attr[0].val.cooperative = 1;
+  } else {
+    static const char* pdl_env = getenv("SPD_NO_PDL");
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_env ? 0 : 1;
+  }
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cuda_err(cudaLaunchKernelEx(&cfg, kern, sp), "spider_step_kernel launch");
