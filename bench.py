@@ -198,16 +198,18 @@ def run_reference(args, cfg_name):
     dense = rng.uniform(-1, 1, tuple(s + 2 * r for s in shape))
     threads = cpu_threads()
     points = int(np.prod(shape))
-    # one bench step = one timestep over the full grid (a bounded sample of
-    # the T-timestep workload; the rate is per timestep like ours)
+    # one bench step = `ts` timesteps over the full grid in one call (a
+    # bounded sample of the T-timestep workload, ~5e8 point updates, so the
+    # per-call grid copies of the C port are amortised like the workload's)
+    ts = max(1, min(T, int(round(5e8 / points))))
     for _ in range(args.warmup):
-        cnaive.naive_apply(coeffs, d, r, dense, r, 1, threads=threads)
+        cnaive.naive_apply(coeffs, d, r, dense, r, ts, threads=threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cnaive.naive_apply(coeffs, d, r, dense, r, 1, threads=threads)
+        cnaive.naive_apply(coeffs, d, r, dense, r, ts, threads=threads)
     el = time.perf_counter() - t0
-    value = points * args.steps * args.gpus / el / 1e9 if False else points * args.steps / el / 1e9
-    sample = f"{shape} grid x 1 timestep per step ({args.steps} steps), fp64, {cpu_model()}"
+    value = points * ts * args.steps / el / 1e9
+    sample = f"{shape} grid x {ts} timestep(s) per step ({args.steps} steps), fp64, {cpu_model()}"
     line = {
         "impl": "reference",
         "metric": f"GStencil/s ({desc})",

@@ -1011,29 +1011,18 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       if (warp == 0 && lane == 0) SPD_TRACE(8, it);
       // Per 32-column batch: pack chunk pairs to 16-bit, xor-butterfly inside
       // the L-lane group so each lane ends up owning 2*PPD consecutive chunks
-      // (32 points = 64 B), then two 256-bit full-line stores.  TMEM loads are
-      // double-buffered: batch cb+1 is in flight while cb is transposed.
+      // (32 points = 64 B), then two 256-bit full-line stores.  Batches go in
+      // pairs: the two butterflies are independent shuffle chains the
+      // scheduler interleaves (the epilogue is latency-bound), and the TMEM
+      // load of the next batch is in flight while the current one is packed.
       constexpr int NB = NTILE / 32;
+      static_assert(NB % 2 == 0, "epilogue processes batch pairs");
       constexpr int PPD = 16 / L;  // packed words (chunk pairs) per destination lane
       const uint32_t tcol = lane_base + C::ACC_COL + acc * NTILE;
-      uint32_t va[32], vb[32];
-      tmem_ld_x32(tcol, va);
-      tmem_wait_ld();
-#pragma unroll
-      for (int cb = 0; cb < NB; ++cb) {
-        uint32_t(&v)[32] = (cb & 1) ? vb : va;
-        uint32_t(&vn)[32] = (cb & 1) ? va : vb;
-        if (cb + 1 < NB) tmem_ld_x32(tcol + (cb + 1) * 32, vn);
-        if (cb == NB - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
-        }
-        if (warp == 0 && lane == 0 && cb == 0) SPD_TRACE(10, it);
-        // bw[k*L + dd] = chunk pair (2j, 2j+1), j = dd*PPD + k, destined to
-        // lane dd of the group.  With the sigma column order (CPL = 2) chunk
-        // 2j sits at column (j/8)*16 + j%8 and chunk 2j+1 eight columns later.
-        uint32_t bw[16];
+      // bw[k*L + dd] = chunk pair (2j, 2j+1), j = dd*PPD + k, destined to
+      // lane dd of the group.  With the sigma column order (CPL = 2) chunk
+      // 2j sits at column (j/8)*16 + j%8 and chunk 2j+1 eight columns later.
+      auto pack = [&](const uint32_t(&v)[32], uint32_t(&bw)[16]) {
 #pragma unroll
         for (int dd = 0; dd < L; ++dd)
 #pragma unroll
@@ -1043,6 +1032,55 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             const int c1 = C::CPL == 2 ? c0 + 8 : 2 * j + 1;
             bw[k * L + dd] = Cvt<T>::pack(__uint_as_float(v[c0]), __uint_as_float(v[c1]));
           }
+      };
+      // lane d ends with bw[k*L + s] = source lane s's pair (chunks
+      // 2(d*PPD+k), +1): 2*PPD consecutive chunks from c_lane; the 16 output
+      // words (x = L*chunk + s, pairs of s) in ascending x.
+      auto store = [&](int cb, const uint32_t(&bw)[16]) {
+        if (!row_ok || (p.dbg & 1)) return;
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < PPD; ++k)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int u = 0; u < L / 2; ++u)
+              w[(2 * k + h) * (L / 2) + u] =
+                  __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
+        const int64_t c_lane = (int64_t)cb * 32 + 2 * PPD * d;
+        T* dst = orow + c_lane * L;
+        if (c_lane + 2 * PPD <= chunk_lim) {
+          stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+          stg_v8(dst + 16, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2 * PPD; ++c) {
+            if (c_lane + c < chunk_lim) {
+              if (L == 4) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(w[2 * c], w[2 * c + 1]);
+              else *reinterpret_cast<uint4*>(dst + c * L) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+            }
+          }
+        }
+      };
+      uint32_t va[32], vb[32];
+      uint32_t b0[16], b1[16];
+      tmem_ld_x32(tcol, va);
+      tmem_wait_ld();
+#pragma unroll
+      for (int pr = 0; pr < NB / 2; ++pr) {
+        const int cb0 = 2 * pr, cb1 = 2 * pr + 1;
+        tmem_ld_x32(tcol + cb1 * 32, vb);
+        if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(10, it);
+        pack(va, b0);
+        tmem_wait_ld();
+        if (cb1 + 1 < NB) tmem_ld_x32(tcol + (cb1 + 1) * 32, va);
+        pack(vb, b1);
+        if (pr == NB / 2 - 1) {
+          // every accumulator column is in registers: free the stage
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
+        }
 #pragma unroll
         for (int b = 1; b < L; b <<= 1) {
           if (p.dbg & 16) break;
@@ -1052,44 +1090,25 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 #pragma unroll
             for (int dd = 0; dd < L; ++dd) {
               if (dd & b) continue;
-              const uint32_t send = upper ? bw[k * L + dd] : bw[k * L + (dd | b)];
-              const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, b);
-              if (upper) bw[k * L + dd] = recv;
-              else bw[k * L + (dd | b)] = recv;
-            }
-          }
-        }
-        if (warp == 0 && lane == 0 && cb == 0) SPD_TRACE(11, it);
-        // lane d now holds bw[k*L + s] = source lane s's pair (chunks 2(d*PPD+k),
-        // +1): 2*PPD consecutive chunks from c_lane; build the 16 output words
-        // (x = L*chunk + s, pairs of s) in ascending x.
-        if (row_ok && !(p.dbg & 1)) {
-          uint32_t w[16];
-#pragma unroll
-          for (int k = 0; k < PPD; ++k)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-              for (int u = 0; u < L / 2; ++u)
-                w[(2 * k + h) * (L / 2) + u] =
-                    __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
-          const int64_t c_lane = (int64_t)cb * 32 + 2 * PPD * d;
-          T* dst = orow + c_lane * L;
-          if (c_lane + 2 * PPD <= chunk_lim) {
-            stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
-            stg_v8(dst + 16, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < 2 * PPD; ++c) {
-              if (c_lane + c < chunk_lim) {
-                if (L == 4) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(w[2 * c], w[2 * c + 1]);
-                else *reinterpret_cast<uint4*>(dst + c * L) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+              const uint32_t s0 = upper ? b0[k * L + dd] : b0[k * L + (dd | b)];
+              const uint32_t s1 = upper ? b1[k * L + dd] : b1[k * L + (dd | b)];
+              const uint32_t r0 = __shfl_xor_sync(0xffffffffu, s0, b);
+              const uint32_t r1 = __shfl_xor_sync(0xffffffffu, s1, b);
+              if (upper) {
+                b0[k * L + dd] = r0;
+                b1[k * L + dd] = r1;
+              } else {
+                b0[k * L + (dd | b)] = r0;
+                b1[k * L + (dd | b)] = r1;
               }
             }
           }
         }
-        if (warp == 0 && lane == 0 && cb == 0) SPD_TRACE(12, it);
-        if (cb + 1 < NB) tmem_wait_ld();
+        if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(11, it);
+        store(cb0, b0);
+        store(cb1, b1);
+        if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(12, it);
+        if (cb1 + 1 < NB) tmem_wait_ld();
       }
       if (warp == 0 && lane == 0) SPD_TRACE(9, it);
       if (p.steps > 1) {
