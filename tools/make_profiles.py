@@ -14,7 +14,21 @@ out.mkdir(exist_ok=True)
 traffic = json.loads((out / "ncu_traffic.json").read_text()) if (out / "ncu_traffic.json").exists() else {}
 for c in configs:
     rep = ROOT / "gpurun_out" / f"prof_{c}_{tag}.ncu-rep"
-    if rep.exists():
+    summ = ROOT / "gpurun_out" / f"ncusum_{c}_{tag}.txt"
+    if not rep.exists() and summ.exists():
+        # summary written on the GPU box (the report itself was not brought back)
+        text = summ.read_text()
+        (out / f"{tag}_ncu_{c}.txt").write_text(f"== ncu --set full, {c}, round tag {tag} (one step kernel launch)\n" + text)
+        vals = {}
+        for ln in text.splitlines():
+            parts = ln.split()
+            if len(parts) >= 3 and parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                vals[parts[0]] = float(parts[1]) * {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1}[parts[2]]
+        if len(vals) == 2:
+            rd, wr = vals["dram__bytes_read.sum"], vals["dram__bytes_write.sum"]
+            traffic[c] = {"dram_bytes_per_launch": int(rd + wr), "read": int(rd), "write": int(wr),
+                          "source": f"profiles/{tag}_ncu_{c}.txt (dram__bytes_read.sum + dram__bytes_write.sum)"}
+    elif rep.exists():
         m = ns.raw(str(rep))
         lines = [f"== ncu --set full, {c}, round tag {tag} (one step kernel launch)"]
         for k in ns.KEYS:
