@@ -221,6 +221,8 @@ int build_geometry(int d, int r, Geometry* g) {
   }
   g->rows_per_mma = 4 / g->kc;
   g->r_out = 128 / L;
+  g->m_tiles = 1;
+  g->mt_rows = 0;
   int rin = 0;
   if (d == 2) {
     g->tile_z = 1;
@@ -239,11 +241,18 @@ int build_geometry(int d, int r, Geometry* g) {
       ++rin;
     }
   } else if (d == 3) {
-    g->tile_z = 4;
+    // Two M = 128 tiles (4 z-planes x 8 rows each) share one 8z x 8y input
+    // block: 100 input rows for 64 output rows (1.56x) instead of 60 per 32
+    // (1.875x).  M-tile 1 uses M-tile 0's MMA schedule and A/E images with
+    // the B rows shifted by 4 planes (40 rows).  N = 32 chunks keeps two B
+    // stages and four natural-row stages in shared memory.
+    g->m_tiles = 2;
+    g->tile_z = 8;
     g->tile_y = 8;
-    g->n_tile = 64;
+    g->n_tile = 32;
     g->tile_x = g->n_tile * L;
-    for (int a = 0; a < g->r_out; ++a) {
+    g->mt_rows = (g->tile_z / g->m_tiles) * (g->tile_y + 2 * r);
+    for (int a = 0; a < g->r_out * g->m_tiles; ++a) {
       g->out_dz[a] = a / g->tile_y;
       g->out_dy[a] = a % g->tile_y;
       g->out_dx[a] = 0;
@@ -286,8 +295,9 @@ int build_geometry(int d, int r, Geometry* g) {
   // an overlapping window whose leading rows carry zero coefficients.
   int rpm = g->rows_per_mma;
   int s = 0;
-  for (int b0 = 0; b0 < rin; b0 += rpm) {
-    int start = b0 + rpm <= rin ? b0 : rin - rpm;
+  const int rin_mma = rin - (g->m_tiles - 1) * g->mt_rows;  // M-tile 0's input rows
+  for (int b0 = 0; b0 < rin_mma; b0 += rpm) {
+    int start = b0 + rpm <= rin_mma ? b0 : rin_mma - rpm;
     g->start_row[s] = start;
     g->first_owned[s] = b0;  // rows [first_owned, start+rpm) belong to MMA s
     ++s;

@@ -255,6 +255,12 @@ struct StepParams {
 // Epilogue: kEpiGroups groups of 4 warps (one warp per TMEM lane quadrant);
 // group g drains the accumulators of the tiles it == g (mod kEpiGroups), so
 // the TMEM -> register -> global path of consecutive tiles overlaps.
+#ifndef SPD_3D_NNAT
+#define SPD_3D_NNAT 4  // 3D natural-row stages (tools/build_variant.sh scans)
+#endif
+#ifndef SPD_3D_NACC
+#define SPD_3D_NACC 4
+#endif
 #ifndef SPD_EPI_GROUPS
 #define SPD_EPI_GROUPS 1
 #endif
@@ -277,7 +283,7 @@ constexpr int kThreads = 32 * (kPollWarp + 1);
 constexpr int kDQ = 8;                   // poller -> loader ring depth
 constexpr int kNPub = 8;                 // publish ring depth (max tiles per publish batch)
 
-template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
+template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0>
 struct Cfg {
   // fast paths: L = 4 (r = 1) and L = 8 (r = 3); any other even L up to 16 uses
   // the generic producer / epilogue
@@ -285,7 +291,10 @@ struct Cfg {
   static constexpr int KC = (2 * L + 7) / 8 <= 1 ? 1 : ((2 * L + 7) / 8 <= 2 ? 2 : 4);
   static constexpr int CPL = GEN ? 1 : 8 / L;  // chunks per lane
   static constexpr int SEG = 32 * CPL;       // chunks per warp segment (256 points)
-  static constexpr int SEGS = NTILE / SEG;   // segments per tile row
+  // HALF: tile rows of 32 chunks (128 points, the 3D two-M-tile geometry):
+  // a warp item is a row pair, one row per half-warp
+  static constexpr bool HALF = !GEN && CPL == 2 && NTILE == 32;
+  static constexpr int SEGS = HALF ? 1 : NTILE / SEG;   // segments per tile row
   // natural row segment staged by the bulk copy: [x0 - 8, x0 + NTILE*L + 8)
   static constexpr int ROW_ELEMS = NTILE * L + 16;
   static constexpr int ROW_BYTES = ROW_ELEMS * 2;
@@ -299,14 +308,20 @@ struct Cfg {
   static constexpr int STG_PITCH = 64 * L + 16;
   static constexpr int STG_BYTES = GEN ? 2 * R_OUT * STG_PITCH + 16 * R_OUT + 16 : 0;
   static constexpr int ACC_COL = 0;
-  static constexpr int E_COL = NACC * NTILE;
+  // MT M-tiles per tile (each M = 128): accumulator stage = MT x NTILE columns
+  static constexpr int ACC_STAGE = MT * NTILE;
+  static constexpr int E_COL = NACC * ACC_STAGE;
   // E for MMA s at E_COL + 2s: bit 0 of the metadata TMEM address is the
   // sparse_id2 selector, so each MMA's column must be even (odd -> misaligned).
   static constexpr int A_COL = E_COL + 2 * SPD_MAX_S;
   static constexpr int TMEM_COLS = 512;  // host checks A_COL + 8*S <= 512
-  static_assert(NTILE % SEG == 0, "tile width must be whole warp segments");
-  // producer work items (input row x warp segment) and items per producer warp
-  static constexpr int N_ITEMS = RIN * SEGS;
+  static_assert(HALF || NTILE % SEG == 0, "tile width must be whole warp segments");
+  // producer work items (input row x warp segment, or row pair) per tile
+  static constexpr int N_ITEMS = HALF ? RIN / 2 : RIN * SEGS;
+  static_assert(!HALF || RIN % 2 == 0, "row pairs");
+  // MMA schedule: the first M-tile's input rows; M-tile t uses them shifted
+  // by t*MTR rows (same A/E images)
+  static constexpr int RIN_MMA = RIN - (MT - 1) * MTR;
   static constexpr int NQ = (N_ITEMS + kProdWarps - 1) / kProdWarps;
 };
 
@@ -387,9 +402,9 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 //   loader --(nat_full: tx bytes)--> producers --(nat_empty)--> loader
 //   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
 //   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0>
 __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR>;
   constexpr int KC = C::KC;
   constexpr int NQ = C::NQ;
   const Geometry& g = p.g;
@@ -671,9 +686,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       }
     } else {
     const int pw = warp - kEpiAll;
-    constexpr int n_items = RIN * C::SEGS;
+    constexpr int n_items = C::N_ITEMS;
     static_assert((NQ - 1) * kProdWarps < n_items && NQ * kProdWarps >= n_items, "NQ must cover the items");
     constexpr int R = (L - 2) / 2;
+    // lane position in its row segment (HALF: row pairs, one per half-warp)
+    constexpr int SW = C::HALF ? 16 : 32;  // lanes per row segment (shuffle width)
+    const int lpos = lane % SW;
     // ext[] words actually referenced by the windows (compile time):
     //   element e of ext is x = 8*lane - 8 + e; windows span
     //   e in [8 - R, 8 + (CPL-1)*L - R + 2L - 1]
@@ -700,12 +718,13 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     for (int q = 0; q < NQ; ++q) {
       const int item = pw + q * kProdWarps;
       valid[q] = q < NQ - 1 || item < n_items;  // only the last slot can be empty
-      const int b = valid[q] ? item / C::SEGS : 0, sg = valid[q] ? item % C::SEGS : 0;
-      const int xl = 8 + sg * 256 + lane * 8;  // this lane's 8 points (stage-local x)
+      const int b = !valid[q] ? 0 : (C::HALF ? 2 * item + lane / 16 : item / C::SEGS);
+      const int sg = (valid[q] && !C::HALF) ? item % C::SEGS : 0;
+      const int xl = 8 + sg * 256 + lpos * 8;  // this lane's 8 points (stage-local x)
       noff[q] = nat_addr(b, xl);
       poff[q] = nat_addr(b, xl - 8) + 4 * kPrevW;
       xoff_n[q] = nat_addr(b, xl + 8);
-      const int n0 = sg * C::SEG + lane * C::CPL;
+      const int n0 = sg * C::SEG + lpos * C::CPL;
       const int col = C::CPL == 2 ? ((n0 & ~15) | ((n0 >> 1) & 7)) : n0;
       soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(col / 8) * sbo + (col % 8) * 16;
     }
@@ -724,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       // phase 1: all shared-memory reads of the tile (ILP across items)
       uint4 cur[NQ];
       uint32_t edge[NQ][kEW];
-      const bool l0 = lane == 0, l31 = lane == 31;
+      const bool l0 = lpos == 0, l31 = lpos == SW - 1;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         if (valid[q] && !(p.dbg & 4)) {
@@ -750,12 +769,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           for (int w = 0; w < 4; ++w) ext[4 + w] = cw[w];
 #pragma unroll
           for (int w = kPrevW; w < 4; ++w) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, cw[w], 1);
+            const uint32_t v = __shfl_up_sync(0xffffffffu, cw[w], 1, SW);
             ext[w] = l0 ? edge[q][w - kPrevW] : v;
           }
 #pragma unroll
           for (int w = 0; w <= kNextW; ++w) {
-            const uint32_t v = __shfl_down_sync(0xffffffffu, cw[w], 1);
+            const uint32_t v = __shfl_down_sync(0xffffffffu, cw[w], 1, SW);
             ext[8 + w] = l31 ? edge[q][w] : v;
           }
           const uint32_t a0 = sbase + soff[q];
@@ -846,7 +865,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     // RIN-RPM), aot.cpp build_geometry).
     const uint32_t idesc = idesc_sparse_f16(128, NTILE, std::is_same<T, __nv_bfloat16>::value);
     constexpr int RPM = 4 / KC;
-    constexpr int S_CT = (RIN + RPM - 1) / RPM;
+    constexpr int RIN_MMA = C::RIN_MMA;
+    constexpr int S_CT = (RIN_MMA + RPM - 1) / RPM;
     int it = 0;
     for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
@@ -859,14 +879,18 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       tc_fence_after();
       if (lane == 0) SPD_TRACE(7, it);
       const uint32_t sbase = bimg_s + stage * stage_bytes;
-      const uint32_t dcol = tmem + C::ACC_COL + acc * NTILE;
+      const uint32_t dcol = tmem + C::ACC_COL + acc * C::ACC_STAGE;
       const uint64_t bdesc0 = umma_desc(sbase, 128, sbo);
 #pragma unroll
-      for (int s = 0; s < S_CT; ++s) {
-        const int start = s * RPM + RPM <= RIN ? s * RPM : RIN - RPM;
-        // descriptor start address field is addr >> 4
-        const uint64_t bdesc = bdesc0 + (uint64_t)((start * KC * 128) >> 4);
-        mma_sp_ts_elect(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
+      for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int s = 0; s < S_CT; ++s) {
+          const int start = (s * RPM + RPM <= RIN_MMA ? s * RPM : RIN_MMA - RPM) + mt * MTR;
+          // descriptor start address field is addr >> 4
+          const uint64_t bdesc = bdesc0 + (uint64_t)((start * KC * 128) >> 4);
+          mma_sp_ts_elect(dcol + mt * NTILE, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc,
+                          s > 0 ? 1u : 0u);
+        }
       }
       tc_commit_elect(bar_empty + 8 * stage);
       tc_commit_elect(bar_accf + 8 * acc);
@@ -913,7 +937,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
         mbar_wait(bar_accf + 8 * acc, aphase);
         tc_fence_after();
-        const uint32_t tcol = lane_base + C::ACC_COL + acc * NTILE;
+        const uint32_t tcol = lane_base + C::ACC_COL + acc * C::ACC_STAGE;
         uint32_t va[32], vb[32];
         tmem_ld_x32(tcol, va);
         tmem_wait_ld();
@@ -984,7 +1008,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const int alpha = m / L;         // output row of the tile
     const int d = lane % L;          // position in the L-lane group
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-    const int odz = g.out_dz[alpha], ody = g.out_dy[alpha], odx = g.out_dx[alpha];
+    // output row of this lane in each M-tile (M-tile t holds rows alpha + t*R_OUT)
+    int odz[MT], ody[MT], odx[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      odz[mt] = g.out_dz[alpha + mt * C::R_OUT];
+      ody[mt] = g.out_dy[alpha + mt * C::R_OUT];
+      odx[mt] = g.out_dx[alpha + mt * C::R_OUT];
+    }
     int it = 0;
     int2 e_nx = fetch(blockIdx.x);
     int e_gi = blockIdx.x;
@@ -997,15 +1028,20 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       e_gi = gi + gridDim.x;
       const TileId id = decode_e(gi, e_cur);
       T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
-      const int64_t z = id.z0 + odz;
-      const int64_t y = id.y0 + ody;
-      const int64_t xr = id.x0 + odx;  // x of chunk 0 of this row
-      bool row_ok;
-      if (g.d == 3) row_ok = z >= p.row_lo && z < p.row_hi && y < p.ny;
-      else if (g.d == 2) row_ok = y >= p.row_lo && y < p.row_hi;
-      else row_ok = true;
-      const int64_t chunk_lim = (p.nx - xr) / L;  // valid chunks in this row
-      T* orow = out + p.origin + z * p.plane + y * p.pitch + xr;
+      bool row_ok[MT];
+      int64_t chunk_lim[MT];  // valid chunks in this row
+      T* orow[MT];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int64_t z = id.z0 + odz[mt];
+        const int64_t y = id.y0 + ody[mt];
+        const int64_t xr = id.x0 + odx[mt];  // x of chunk 0 of this row
+        if (g.d == 3) row_ok[mt] = z >= p.row_lo && z < p.row_hi && y < p.ny;
+        else if (g.d == 2) row_ok[mt] = y >= p.row_lo && y < p.row_hi;
+        else row_ok[mt] = true;
+        chunk_lim[mt] = (p.nx - xr) / L;
+        orow[mt] = out + p.origin + z * p.plane + y * p.pitch + xr;
+      }
       mbar_wait(bar_accf + 8 * acc, aphase);
       tc_fence_after();
       if (warp == 0 && lane == 0) SPD_TRACE(8, it);
@@ -1015,10 +1051,11 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       // pairs: the two butterflies are independent shuffle chains the
       // scheduler interleaves (the epilogue is latency-bound), and the TMEM
       // load of the next batch is in flight while the current one is packed.
-      constexpr int NB = NTILE / 32;
-      static_assert(NB % 2 == 0, "epilogue processes batch pairs");
+      constexpr int NB = NTILE / 32;  // batches per M-tile
+      constexpr int TB = MT * NB;     // batches per tile (batch bi: M-tile bi / NB, column batch bi % NB)
+      static_assert(TB % 2 == 0, "epilogue processes batch pairs");
       constexpr int PPD = 16 / L;  // packed words (chunk pairs) per destination lane
-      const uint32_t tcol = lane_base + C::ACC_COL + acc * NTILE;
+      const uint32_t tcol = lane_base + C::ACC_COL + acc * C::ACC_STAGE;  // batch bi at tcol + 32 bi
       // bw[k*L + dd] = chunk pair (2j, 2j+1), j = dd*PPD + k, destined to
       // lane dd of the group.  With the sigma column order (CPL = 2) chunk
       // 2j sits at column (j/8)*16 + j%8 and chunk 2j+1 eight columns later.
@@ -1036,8 +1073,9 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       // lane d ends with bw[k*L + s] = source lane s's pair (chunks
       // 2(d*PPD+k), +1): 2*PPD consecutive chunks from c_lane; the 16 output
       // words (x = L*chunk + s, pairs of s) in ascending x.
-      auto store = [&](int cb, const uint32_t(&bw)[16]) {
-        if (!row_ok || (p.dbg & 1)) return;
+      auto store = [&](int bi, const uint32_t(&bw)[16]) {
+        const int mt = bi / NB, cb = bi % NB;
+        if (!row_ok[mt] || (p.dbg & 1)) return;
         uint32_t w[16];
 #pragma unroll
         for (int k = 0; k < PPD; ++k)
@@ -1048,14 +1086,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
               w[(2 * k + h) * (L / 2) + u] =
                   __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
         const int64_t c_lane = (int64_t)cb * 32 + 2 * PPD * d;
-        T* dst = orow + c_lane * L;
-        if (c_lane + 2 * PPD <= chunk_lim) {
+        T* dst = orow[mt] + c_lane * L;
+        if (c_lane + 2 * PPD <= chunk_lim[mt]) {
           stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
           stg_v8(dst + 16, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
         } else {
 #pragma unroll
           for (int c = 0; c < 2 * PPD; ++c) {
-            if (c_lane + c < chunk_lim) {
+            if (c_lane + c < chunk_lim[mt]) {
               if (L == 4) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(w[2 * c], w[2 * c + 1]);
               else *reinterpret_cast<uint4*>(dst + c * L) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
             }
@@ -1067,15 +1105,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       tmem_ld_x32(tcol, va);
       tmem_wait_ld();
 #pragma unroll
-      for (int pr = 0; pr < NB / 2; ++pr) {
+      for (int pr = 0; pr < TB / 2; ++pr) {
         const int cb0 = 2 * pr, cb1 = 2 * pr + 1;
         tmem_ld_x32(tcol + cb1 * 32, vb);
         if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(10, it);
         pack(va, b0);
         tmem_wait_ld();
-        if (cb1 + 1 < NB) tmem_ld_x32(tcol + (cb1 + 1) * 32, va);
+        if (cb1 + 1 < TB) tmem_ld_x32(tcol + (cb1 + 1) * 32, va);
         pack(vb, b1);
-        if (pr == NB / 2 - 1) {
+        if (pr == TB / 2 - 1) {
           // every accumulator column is in registers: free the stage
           tc_fence_before();
           __syncwarp();
@@ -1108,7 +1146,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         store(cb0, b0);
         store(cb1, b1);
         if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(12, it);
-        if (cb1 + 1 < NB) tmem_wait_ld();
+        if (cb1 + 1 < TB) tmem_wait_ld();
       }
       if (warp == 0 && lane == 0) SPD_TRACE(9, it);
       if (p.steps > 1) {
@@ -1332,16 +1370,19 @@ static int plan_counters(const spd_plan* cplan, int n, cudaStream_t st, unsigned
   return cuda_err(cudaMemsetAsync(plan->d_counters, 0, sizeof(unsigned int) * n, st), "counter reset");
 }
 
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN>;
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR>;
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
   {  // the MMA issuer's compile-time schedule must be the plan's
     constexpr int RPM = 4 / C::KC;
-    if (plan->g.s != (RIN + RPM - 1) / RPM) return set_error(SPD_EUNSUPPORTED, "MMA count mismatch (%d)", plan->g.s);
+    constexpr int RM = C::RIN_MMA;
+    if (plan->g.s != (RM + RPM - 1) / RPM) return set_error(SPD_EUNSUPPORTED, "MMA count mismatch (%d)", plan->g.s);
+    if (plan->g.m_tiles != MT || (MT > 1 && plan->g.mt_rows != MTR))
+      return set_error(SPD_EUNSUPPORTED, "M-tile geometry mismatch (%d)", plan->g.m_tiles);
     for (int s = 0; s < plan->g.s; ++s)
-      if (plan->g.start_row[s] != (s * RPM + RPM <= RIN ? s * RPM : RIN - RPM))
+      if (plan->g.start_row[s] != (s * RPM + RPM <= RM ? s * RPM : RM - RPM))
         return set_error(SPD_EUNSUPPORTED, "MMA start row mismatch (%d)", s);
   }
   sp.nat_bytes = sp.use_tmap ? sp.nbox * sp.box_slot : plan->g.r_in * C::ROW_BYTES;
@@ -1392,7 +1433,8 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   // (scan in profiles/r01_tuning.txt).
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 34) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 34>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
-  if (g.L == 4 && g.n_tile == 64 && g.r_in == 60) return launch_step<T, 4, PARITY, 64, 2, 3, 4, 60>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
+    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 22>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16>(plan, sp, st);
   // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
@@ -1693,6 +1735,8 @@ int spd_plan_info(const spd_plan* plan, int32_t* info) {
   info[5] = g.tile_z;
   info[6] = g.tile_y;
   info[7] = g.kc;
+  info[8] = g.m_tiles;
+  info[9] = g.mt_rows;
   return SPD_OK;
 }
 
@@ -1713,7 +1757,7 @@ int spd_plan_geometry(const spd_plan* plan, int32_t* in_off, int32_t* out_off) {
     in_off[3 * b + 1] = g.in_dy[b];
     in_off[3 * b + 2] = g.in_dx[b];
   }
-  for (int a = 0; out_off && a < g.r_out; ++a) {
+  for (int a = 0; out_off && a < g.r_out * g.m_tiles; ++a) {
     out_off[3 * a] = g.out_dz[a];
     out_off[3 * a + 1] = g.out_dy[a];
     out_off[3 * a + 2] = g.out_dx[a];

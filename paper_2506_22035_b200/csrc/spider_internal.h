@@ -9,8 +9,8 @@
 #include "../../include/spider.h"
 
 #define SPD_ABI_VERSION 1
-#define SPD_MAX_RIN 64
-#define SPD_MAX_ROUT 32
+#define SPD_MAX_RIN 128
+#define SPD_MAX_ROUT 64
 #define SPD_MAX_S 24
 
 namespace spd {
@@ -38,7 +38,9 @@ struct Geometry {
   int d, r, L;
   int kc;            // 16-byte K-chunks per input-row window (2L/8 rounded up to 1, 2 or 4)
   int rows_per_mma;  // input rows per K=32 MMA (4/kc)
-  int r_out;         // output rows per tile (128/L)
+  int r_out;         // output rows per M-tile (128/L)
+  int m_tiles;       // M = 128 tiles per tile (3D: 2, sharing one input block)
+  int mt_rows;       // input-row offset between consecutive M-tiles
   int r_in;          // input image rows per tile
   int s;             // MMAs per tile
   int n_tile;        // x-chunks per tile (MMA N)

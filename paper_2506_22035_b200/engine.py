@@ -47,6 +47,8 @@ class PlanInfo:
     tile_z: int
     tile_y: int
     kchunks: int
+    m_tiles: int = 1  # M = 128 tiles per tile (3D: 2, sharing one input block)
+    mt_rows: int = 0  # input-row shift of M-tile t's MMA schedule: t * mt_rows
 
 
 class Plan:
@@ -87,7 +89,7 @@ class Plan:
             pass
 
     def info(self) -> PlanInfo:
-        buf = np.zeros(8, dtype=np.int32)
+        buf = np.zeros(10, dtype=np.int32)
         check(lib.spd_plan_info(self._h, i32ptr(buf)))
         return PlanInfo(*[int(v) for v in buf])
 
@@ -101,10 +103,10 @@ class Plan:
         return a, e, s
 
     def geometry(self):
-        """(in_off [R_in,3], out_off [R_out,3]) tile row offsets (dz, dy, dx)."""
+        """(in_off [R_in,3], out_off [R_out*m_tiles,3]) tile row offsets (dz, dy, dx)."""
         inf = self.info()
         a = np.zeros((inf.r_in, 3), dtype=np.int32)
-        b = np.zeros((inf.r_out, 3), dtype=np.int32)
+        b = np.zeros((inf.r_out * inf.m_tiles, 3), dtype=np.int32)
         check(lib.spd_plan_geometry(self._h, i32ptr(a), i32ptr(b)))
         return a, b
 

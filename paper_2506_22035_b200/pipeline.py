@@ -218,15 +218,15 @@ def _stats(kernel: StencilKernel, grid, steps: int, parity: Parity, plan: Plan) 
     info = plan.info()
     tiles_x = -(-grid.B // (info.n_tile * L)) if kernel.d != 1 else -(-grid.B // (info.n_tile * L * info.r_out))
     tiles = tiles_x * (-(-grid.A // info.tile_y) if kernel.d >= 2 else 1) * (-(-planes // info.tile_z))
-    st.tile_counts = {"block_tiles": tiles, "n_tile": info.n_tile, "tile_rows": info.r_out}
+    st.tile_counts = {"block_tiles": tiles, "n_tile": info.n_tile, "tile_rows": info.r_out * info.m_tiles}
     st.device = {
         "arch": "sm_100a",
         "instruction": "tcgen05.mma.sp.cta_group::1.kind::f16 M128 N%d K32" % info.n_tile,
         "dtype": plan.dtype,
         "launches": steps,
         "tiles_per_step": tiles,
-        "mma_instructions": steps * tiles * info.mmas_per_tile,
-        "issued_sparse_macs": steps * tiles * info.mmas_per_tile * 128 * info.n_tile * 16,
+        "mma_instructions": steps * tiles * info.mmas_per_tile * info.m_tiles,
+        "issued_sparse_macs": steps * tiles * info.mmas_per_tile * info.m_tiles * 128 * info.n_tile * 16,
     }
     return st
 

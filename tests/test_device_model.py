@@ -60,16 +60,20 @@ def tile_model(plan, dense, halo):
                 if 0 <= zz < dense3.shape[0] and 0 <= yy < dense3.shape[1] and 0 <= xx < dense3.shape[2]:
                     Bimg[b, n, q] = dense3[zz, yy, xx]
     rpm = 32 // kslots
-    D = np.zeros((128, n_tile))
-    for s in range(inf.mmas_per_tile):
-        Bs = Bimg[starts[s] : starts[s] + rpm].transpose(0, 2, 1).reshape(32, n_tile)
-        D += A[s] @ Bs
     out = {}
-    for a in range(inf.r_out):
-        dz, dy, dx = out_off[a]
-        for i in range(L):
-            for n in range(n_tile):
-                out[(dz, dy, dx + n * L + i)] = D[L * a + i, n]
+    # M-tile t runs the same MMA schedule (same A/E) on B rows shifted by
+    # t * mt_rows and produces output rows t * r_out ..
+    for t in range(inf.m_tiles):
+        D = np.zeros((128, n_tile))
+        for s in range(inf.mmas_per_tile):
+            b0 = starts[s] + t * inf.mt_rows
+            Bs = Bimg[b0 : b0 + rpm].transpose(0, 2, 1).reshape(32, n_tile)
+            D += A[s] @ Bs
+        for a in range(inf.r_out):
+            dz, dy, dx = out_off[a + t * inf.r_out]
+            for i in range(L):
+                for n in range(n_tile):
+                    out[(dz, dy, dx + n * L + i)] = D[L * a + i, n]
     return out
 
 
