@@ -225,16 +225,18 @@ int build_geometry(int d, int r, Geometry* g) {
   g->mt_rows = 0;
   int rin = 0;
   if (d == 2) {
+    // (Stacking M-tiles to share the input block, as 3D does, was measured
+    // slower for r = 3: 4 M-tiles x N = 32 113 -> 142 us, 2 x 32 -> 119 us.)
     g->tile_z = 1;
-    g->tile_y = g->r_out;
+    g->tile_y = g->r_out * g->m_tiles;
     g->n_tile = (L == 4) ? 128 : 64;
     g->tile_x = g->n_tile * L;
-    for (int a = 0; a < g->r_out; ++a) {
+    for (int a = 0; a < g->r_out * g->m_tiles; ++a) {
       g->out_dz[a] = 0;
       g->out_dy[a] = a;
       g->out_dx[a] = 0;
     }
-    for (int b = 0; b < g->r_out + 2 * r; ++b) {
+    for (int b = 0; b < g->tile_y + 2 * r; ++b) {
       g->in_dz[rin] = 0;
       g->in_dy[rin] = b - r;
       g->in_dx[rin] = 0;
