@@ -153,6 +153,13 @@ int spd_run(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
 int spd_run_ex(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
                void* buf1, int steps, int flags, void* stream);
 
+/* One step over the first and the last tile band (2D: tile rows, 3D: tile
+ * planes) of the grid in a single launch: a slab's boundary bands, computed
+ * before its halo exchange (replaces two spd_step_range calls; the rest is
+ * spd_step_range over the interior bands).  2D / 3D only. */
+int spd_step_edges(const spd_plan* plan, const spd_grid_desc* g, const void* in,
+                   void* out, void* stream);
+
 /* One step restricted to output rows [y_begin, y_end) (2D) or planes
  * [z_begin, z_end) (3D) — used by the slab driver to compute the boundary
  * bands before the halo exchange and the interior after. */

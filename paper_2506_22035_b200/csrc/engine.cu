@@ -243,6 +243,8 @@ struct StepParams {
   int64_t ny;                // 3D: y extent (rows beyond it are masked)
   int tiles_x, tiles_y, tiles_z;
   int tile_y0, tile_z0;      // first tile row / plane of the range
+  int band_stride;           // tile rows (2D) / planes (3D) between consecutive bands of the range (1, or
+                             // last-first for the two-edge launch of a slab's boundary bands)
   int n_tiles;
   int reverse;               // step 0 traverses tiles last-to-first; steps alternate
   int dbg;                   // development switches (SPD_DBG), 0 in production
@@ -537,8 +539,8 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const int by = rest % p.tiles_y;
     const int bz = rest / p.tiles_y;
     id.x0 = (int64_t)bx * g.tile_x;
-    id.y0 = (int64_t)(p.tile_y0 + by) * g.tile_y;
-    id.z0 = (int64_t)(p.tile_z0 + bz) * g.tile_z;
+    id.y0 = (int64_t)(p.tile_y0 + (g.d == 2 ? by * p.band_stride : by)) * g.tile_y;
+    id.z0 = (int64_t)(p.tile_z0 + bz * p.band_stride) * g.tile_z;
     id.band = g.d == 3 ? bz : (g.d == 2 ? by : bx);
     return id;
   };
@@ -1549,6 +1551,7 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     sp.row_hi = 1;
     sp.tiles_y = sp.tiles_z = 1;
   }
+  sp.band_stride = 1;
   sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
   if (g.d == 3) {
     sp.n_bands = sp.tiles_z;
@@ -1821,6 +1824,25 @@ int spd_step_range(const spd_plan* plan, const spd_grid_desc* gd, const void* in
   StepParams sp;
   rc = fill_step_params(plan, gd, in, out, lo, hi, 1, sp);
   if (rc) return rc;
+  return dispatch(plan, sp, (cudaStream_t)stream);
+}
+
+int spd_step_edges(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, void* stream) {
+  using namespace spd;
+  int rc = check_desc(plan, gd);
+  if (rc) return rc;
+  if (plan->d == 1) return set_error(SPD_EINVAL, "edge bands are defined for 2D / 3D grids");
+  const int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
+  StepParams sp;
+  rc = fill_step_params(plan, gd, in, out, 0, extent, 1, sp);
+  if (rc) return rc;
+  int& nb = plan->d == 3 ? sp.tiles_z : sp.tiles_y;
+  if (nb > 2) {  // first and last tile band only, one launch
+    sp.band_stride = nb - 1;
+    nb = 2;
+    sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
+    sp.n_bands = 2;
+  }
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
 

@@ -113,17 +113,27 @@ class SlabDriver:
         self.compute_stream = compute_stream
 
     def _bands(self):
+        """(boundary, interior) row ranges: the first and the last tile band,
+        and everything between (slab boundaries are tile-aligned except the
+        global bottom, which exchanges nothing downward)."""
         rows, band = self.ops.rows, self.ops.band
-        if rows <= 2 * band:
+        last = ((rows - 1) // band) * band  # first row of the last tile band
+        if last <= band:
             return [(0, rows)], []
-        return [(0, band), (rows - band, rows)], [(band, rows - band)]
+        return [(0, band), (last, rows)], [(band, last)]
+
+    def _compute_boundary(self, boundary) -> None:
+        if len(boundary) == 2 and hasattr(self.ops, "compute_edges"):
+            self.ops.compute_edges()  # both edge bands in one launch
+        else:
+            for lo, hi in boundary:
+                self.ops.compute(lo, hi)
 
     def step(self) -> None:
         """One timestep: boundary bands, exchange (overlapped on the comm
         stream when CUDA), interior bands, flip."""
         boundary, interior = self._bands()
-        for lo, hi in boundary:
-            self.ops.compute(lo, hi)
+        self._compute_boundary(boundary)
         if self.comm_stream is not None:
             done = torch.cuda.Event()
             done.record(self.compute_stream)
@@ -143,8 +153,7 @@ class SlabDriver:
 
     # phase API (used to emulate several ranks in one process)
     def step_boundary(self) -> None:
-        for lo, hi in self._bands()[0]:
-            self.ops.compute(lo, hi)
+        self._compute_boundary(self._bands()[0])
 
     def pack_messages(self) -> None:
         m, s = self.msgs, self.slab
@@ -196,6 +205,9 @@ class DeviceSlabOps(SlabOps):
 
     def compute(self, lo: int, hi: int) -> None:
         self.grid.step_range(lo, hi, self.stream)
+
+    def compute_edges(self) -> None:
+        self.grid.step_edges(self.stream)
 
     def flip(self) -> None:
         self.grid.flip()

@@ -196,6 +196,13 @@ class DeviceGrid:
         check(lib.spd_step_range(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()),
                                  C.c_void_p(b.data_ptr()), int(lo), int(hi), _stream_ptr(stream)))
 
+    def step_edges(self, stream=None) -> None:
+        """One step over the first and last tile bands only (one launch); with
+        step_range over the bands between them this is a full step."""
+        a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
+        check(lib.spd_step_edges(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()),
+                                 C.c_void_p(b.data_ptr()), _stream_ptr(stream)))
+
     def flip(self) -> None:
         self.cur = 1 - self.cur
         self.step += 1

@@ -424,3 +424,27 @@ def test_cli_run_and_verify_on_device(tmp_path, capsys):
     assert cli.main(["verify", "--kernel", str(gold / "box2d_r3.json"), "--sizes", "48,80", "--steps", "1"]) == cli.EXIT_OK
     out = capsys.readouterr().out
     assert "all_pass:" in out
+
+
+@pytest.mark.parametrize("d,shape", [(2, (130, 512)), (2, (96, 1024)), (3, (20, 24, 256)), (3, (40, 16, 128))])
+def test_step_edges_plus_interior_is_a_full_step(d, shape):
+    """The slab driver's boundary launch (first + last tile band in one
+    launch, spd_step_edges) plus the interior range is one full step, bit for
+    bit."""
+    k = rand_kernel("box", d, 1, seed=[d, 3])
+    plan = get_plan(k, sp.Parity.EVEN, "fp16")
+    inf = plan.info()
+    band = inf.tile_z if d == 3 else inf.tile_y
+    dense = torch.rand(tuple(n + 2 for n in shape), dtype=torch.float64, device="cuda")
+    a = DeviceGrid(plan, shape, 1)
+    b = DeviceGrid(plan, shape, 1)
+    a.load_dense_f64(dense)
+    b.load_dense_f64(dense)
+    a.run(1)
+    b.step_edges()
+    rows = shape[0]
+    last = ((rows - 1) // band) * band
+    if last > band:
+        b.step_range(band, last)
+    b.flip()
+    assert torch.equal(a.bufs[a.cur], b.bufs[b.cur])
