@@ -1066,15 +1066,20 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         for (int dd = 0; dd < L; ++dd)
 #pragma unroll
           for (int k = 0; k < PPD; ++k) {
-            const int j = dd * PPD + k;
+            // destination lane dd owns chunk pairs dd*PPD/2 + [0, PPD/2) of
+            // each half batch (16 chunks): two 32-byte pieces 16 chunks apart,
+            // so each 256-bit store instruction of the warp writes whole
+            // 128-byte lines (4 or 8 lanes side by side)
+            const int j = (k < PPD / 2 ? 0 : 8) + dd * (PPD / 2) + k % (PPD / 2);
             const int c0 = C::CPL == 2 ? (j / 8) * 16 + (j % 8) : 2 * j;
             const int c1 = C::CPL == 2 ? c0 + 8 : 2 * j + 1;
             bw[k * L + dd] = Cvt<T>::pack(__uint_as_float(v[c0]), __uint_as_float(v[c1]));
           }
       };
-      // lane d ends with bw[k*L + s] = source lane s's pair (chunks
-      // 2(d*PPD+k), +1): 2*PPD consecutive chunks from c_lane; the 16 output
-      // words (x = L*chunk + s, pairs of s) in ascending x.
+      // lane d ends with bw[k*L + s] = source lane s's pair of chunks for
+      // its pair index k: PPD consecutive chunks at d*PPD and PPD more at
+      // 16 + d*PPD; the 16 output words (x = L*chunk + s, pairs of s), piece
+      // by piece in ascending x.
       auto store = [&](int bi, const uint32_t(&bw)[16]) {
         const int mt = bi / NB, cb = bi % NB;
         if (!row_ok[mt] || (p.dbg & 1)) return;
@@ -1087,17 +1092,19 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             for (int u = 0; u < L / 2; ++u)
               w[(2 * k + h) * (L / 2) + u] =
                   __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
-        const int64_t c_lane = (int64_t)cb * 32 + 2 * PPD * d;
+        const int64_t c_lane = (int64_t)cb * 32 + PPD * d;  // first chunk of piece 0; piece 1 at +16
         T* dst = orow[mt] + c_lane * L;
-        if (c_lane + 2 * PPD <= chunk_lim[mt]) {
+        if (c_lane + 16 + PPD <= chunk_lim[mt]) {
           stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
-          stg_v8(dst + 16, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+          stg_v8(dst + 16 * L, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
         } else {
 #pragma unroll
           for (int c = 0; c < 2 * PPD; ++c) {
-            if (c_lane + c < chunk_lim[mt]) {
-              if (L == 4) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(w[2 * c], w[2 * c + 1]);
-              else *reinterpret_cast<uint4*>(dst + c * L) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+            const int64_t ch = c_lane + (c / PPD) * 16 + c % PPD;
+            if (ch < chunk_lim[mt]) {
+              T* dc = orow[mt] + ch * L;
+              if (L == 4) *reinterpret_cast<uint2*>(dc) = make_uint2(w[2 * c], w[2 * c + 1]);
+              else *reinterpret_cast<uint4*>(dc) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
             }
           }
         }
