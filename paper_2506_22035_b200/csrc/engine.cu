@@ -391,6 +391,13 @@ __device__ __forceinline__ void lds_u32_if(uint32_t& v, bool pred, uint32_t addr
   asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %1, 0;\n@p ld.shared.u32 %0, [%2];\n}" : "+r"(v) : "r"((uint32_t)pred), "r"(addr));
 }
 
+// Predicated 128-bit shared load (v keeps its value where pred is false).
+__device__ __forceinline__ void lds_v4_if(uint4& v, bool pred, uint32_t addr) {
+  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n@p ld.shared.v4.u32 {%0,%1,%2,%3}, [%5];\n}"
+               : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+               : "r"((uint32_t)pred), "r"(addr));
+}
+
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -710,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     // then covers the 32 banks once per quarter-warp — conflict-free without
     // per-lane selects.  The epilogue undoes sigma when it pairs D columns.
     uint32_t noff[NQ], poff[NQ], xoff_n[NQ], soff[NQ];
+    static_assert(kPrevW >= 0 && kPrevW < 4 && kNextW < 4, "edge words must fit one 16-byte block");
     bool valid[NQ];
     // natural stage: element x of row b at box k = x / boxw
     auto nat_addr = [&](int b, int x) -> uint32_t {
@@ -724,15 +732,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       const int sg = (valid[q] && !C::HALF) ? item % C::SEGS : 0;
       const int xl = 8 + sg * 256 + lpos * 8;  // this lane's 8 points (stage-local x)
       noff[q] = nat_addr(b, xl);
-      poff[q] = nat_addr(b, xl - 8) + 4 * kPrevW;
-      xoff_n[q] = nat_addr(b, xl + 8);
+      poff[q] = nat_addr(b, xl - 8);  // 16-B block left of the lane's (segment-start lane)
+      xoff_n[q] = nat_addr(b, xl + 8);  // 16-B block right of it (segment-end lane)
       const int n0 = sg * C::SEG + lpos * C::CPL;
       const int col = C::CPL == 2 ? ((n0 & ~15) | ((n0 >> 1) & 7)) : n0;
       soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(col / 8) * sbo + (col % 8) * 16;
     }
-    constexpr int kPW = 4 - kPrevW;  // prev words needed by lane 0
-    constexpr int kNW = kNextW + 1;  // next words needed by lane 31
-    constexpr int kEW = kPW > kNW ? kPW : kNW;
     int it = 0;
     for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
       const int stage = it % NSTAGE;
@@ -744,18 +749,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       if (pw == 0 && lane == 0) SPD_TRACE(2, it);
       // phase 1: all shared-memory reads of the tile (ILP across items)
       uint4 cur[NQ];
-      uint32_t edge[NQ][kEW];
+      uint4 edge[NQ];  // segment-edge lanes: the neighbouring 16-B block (one predicated load)
       const bool l0 = lpos == 0, l31 = lpos == SW - 1;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
         if (valid[q] && !(p.dbg & 4)) {
           cur[q] = lds_v4(nbase + noff[q]);
-#pragma unroll
-          for (int w = 0; w < kEW; ++w) {
-            edge[q][w] = 0;
-            if (w < kPW) lds_u32_if(edge[q][w], l0, nbase + poff[q] + 4 * w);
-            if (w < kNW) lds_u32_if(edge[q][w], l31, nbase + xoff_n[q] + 4 * w);
-          }
+          edge[q] = make_uint4(0, 0, 0, 0);
+          lds_v4_if(edge[q], l0 || l31, nbase + (l0 ? poff[q] : xoff_n[q]));
         }
       }
       mbar_wait(bar_empty + 8 * stage, sphase ^ 1);
@@ -770,14 +771,16 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 #pragma unroll
           for (int w = 0; w < 4; ++w) ext[4 + w] = cw[w];
 #pragma unroll
+          const uint32_t ew[4] = {edge[q].x, edge[q].y, edge[q].z, edge[q].w};
+#pragma unroll
           for (int w = kPrevW; w < 4; ++w) {
             const uint32_t v = __shfl_up_sync(0xffffffffu, cw[w], 1, SW);
-            ext[w] = l0 ? edge[q][w - kPrevW] : v;
+            ext[w] = l0 ? ew[w] : v;
           }
 #pragma unroll
           for (int w = 0; w <= kNextW; ++w) {
             const uint32_t v = __shfl_down_sync(0xffffffffu, cw[w], 1, SW);
-            ext[8 + w] = l31 ? edge[q][w] : v;
+            ext[8 + w] = l31 ? ew[w] : v;
           }
           const uint32_t a0 = sbase + soff[q];
 #pragma unroll
