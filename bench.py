@@ -246,9 +246,16 @@ def run_ours(args, cfg_name):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # SPD_BENCH_BACKEND=gloo lets several ranks share one GPU (functional
+    # checks of the multi-rank path on a 1-GPU box; timings then mean nothing)
+    backend = os.environ.get("SPD_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     desc, shape, d, r, kind, T = CONFIGS[cfg_name]
     kern = make_kernel(kind, d, r)
     plan = get_plan(kern, sp.Parity.EVEN, "fp16", local)
@@ -258,10 +265,14 @@ def run_ours(args, cfg_name):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     dense_shape = tuple(s + 2 * r for s in shape)
+    peer = None
     if world == 1 and not args.force_slab:
         grid = DeviceGrid(plan, shape, r)
         dense = torch.rand(dense_shape, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
@@ -301,10 +312,24 @@ def run_ours(args, cfg_name):
         drv = SlabDriver(slab, ops, comm_stream=comm, compute_stream=stream)
         boundary, interior = drv._bands()
         launches_per_step = T * (len(boundary) + len(interior))
+        if args.exchange == "peer":
+            # halos through peer memory (CUDA IPC + stream memory operations):
+            # one host call per timestep, no NCCL on the data path
+            from paper_2506_22035_b200.distributed import PeerSlab
+
+            try:
+                peer = PeerSlab(plan, slab, ops.grid, compute_stream=stream, comm_stream=comm)
+            except Exception as exc:  # IPC unavailable: NCCL send/recv driver
+                print(f"peer exchange unavailable ({exc}); using NCCL send/recv", file=sys.stderr)
+                args.exchange = "nccl"
 
         def one_step():
-            for _ in range(T):
-                drv.step()
+            if peer is not None:
+                for _ in range(T):
+                    peer.step()
+            else:
+                for _ in range(T):
+                    drv.step()
 
     for _ in range(args.warmup):
         one_step()
@@ -323,7 +348,7 @@ def run_ours(args, cfg_name):
         barrier()
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
@@ -394,6 +419,7 @@ def run_ours(args, cfg_name):
             "config": {"workload": cfg_name, "description": desc, "grid_per_gpu": list(shape),
                        "timesteps_per_step": T, "parallelism": f"slab{world}" if slab_mode else "single",
                        "launch": "cuda-graph" if args.graph else "stream, programmatic dependent launch",
+                       "exchange": (args.exchange if slab_mode else None),
                        "l2": f"inputs larger than L2 ({2 * np.prod(dense_shape) / 2**20:.0f} MiB per buffer)",
                        "tile": {"L": info.L, "n_tile": info.n_tile, "mmas_per_tile": info.mmas_per_tile},
                        "slab": slab},
@@ -404,6 +430,9 @@ def run_ours(args, cfg_name):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        barrier()
+        peer.close()
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -420,6 +449,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--force-slab", action="store_true", help="use the multi-GPU slab driver even at N=1")
     ap.add_argument("--graph", action="store_true", help="replay the T step launches as one CUDA graph")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N>1 halo exchange: peer memory (CUDA IPC, default) or NCCL send/recv")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

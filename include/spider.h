@@ -207,6 +207,32 @@ int spd_halo_pack(const spd_grid_desc* g, const void* buf, int rows, int dir,
 int spd_halo_unpack(const spd_grid_desc* g, void* buf, int rows, int dir,
                     const void* msg, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Peer-memory slab exchange (one process per GPU, CUDA IPC).
+ * spd_ipc_export: 64-byte IPC handle of the allocation holding ptr and ptr's
+ * byte offset in it; spd_ipc_open maps a handle exported by another process
+ * (returns the pointer and the mapping base for spd_ipc_close).
+ * spd_slab_create: buf0/buf1 this rank's ping-pong grids, my_flags a zeroed
+ * device uint32[2] ([0] written by the up neighbour, [1] by the down one);
+ * the up_ / dn_ arguments are the neighbours' mapped buffers, layouts and flag
+ * words (NULL buffers at the global boundary).
+ * spd_slab_step(t): waits (stream memory op) for the neighbours' step t-1
+ * halos, computes the two boundary tile bands, copies the r outermost rows
+ * into the neighbours' halo rows and bumps their flags on comm_stream, and
+ * computes the interior bands on compute_stream.  The result of step t is in
+ * buf[(t+1) % 2]. */
+int spd_ipc_export(const void* ptr, void* handle64, int64_t* offset);
+int spd_ipc_open(const void* handle64, int64_t offset, void** ptr, void** base);
+int spd_ipc_close(void* base);
+typedef struct spd_slab spd_slab;
+int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, void* buf1,
+                    void* my_flags, void* up_buf0, void* up_buf1,
+                    const spd_grid_desc* up_g, void* up_flags, void* dn_buf0,
+                    void* dn_buf1, const spd_grid_desc* dn_g, void* dn_flags,
+                    spd_slab** out);
+int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream);
+int spd_slab_destroy(spd_slab* s);
+
 #ifdef __cplusplus
 }
 #endif

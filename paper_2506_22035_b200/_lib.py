@@ -84,6 +84,12 @@ SIGNATURES = {
     "spd_mma_selftest": (_I, [_P, _P, _P, _I, _P, _P]),
     "spd_halo_pack": (_I, [_DESC, _P, _I, _I, _P, _P]),
     "spd_halo_unpack": (_I, [_DESC, _P, _I, _I, _P, _P]),
+    "spd_ipc_export": (_I, [_P, _P, _I64P]),
+    "spd_ipc_open": (_I, [_P, C.c_int64, C.POINTER(_P), C.POINTER(_P)]),
+    "spd_ipc_close": (_I, [_P]),
+    "spd_slab_create": (_I, [_P, _DESC, _P, _P, _P, _P, _P, _DESC, _P, _P, _P, _DESC, _P, C.POINTER(_P)]),
+    "spd_slab_step": (_I, [_P, _I, _P, _P]),
+    "spd_slab_destroy": (_I, [_P]),
 }
 
 

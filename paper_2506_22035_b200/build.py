@@ -16,7 +16,7 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libspider.so"
-SOURCES = [CSRC / "engine.cu", CSRC / "aot.cpp"]
+SOURCES = [CSRC / "engine.cu", CSRC / "peer.cu", CSRC / "aot.cpp"]
 HEADERS = [CSRC / "spider_internal.h", HERE.parent / "include" / "spider.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

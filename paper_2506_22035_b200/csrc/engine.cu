@@ -770,7 +770,6 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
 #pragma unroll
           for (int w = 0; w < 4; ++w) ext[4 + w] = cw[w];
-#pragma unroll
           const uint32_t ew[4] = {edge[q].x, edge[q].y, edge[q].z, edge[q].w};
 #pragma unroll
           for (int w = kPrevW; w < 4; ++w) {

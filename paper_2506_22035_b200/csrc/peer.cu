@@ -1,0 +1,247 @@
+// Multi-GPU slab exchange over peer memory ("fuse" option):
+// each rank maps its y/z neighbours' grid buffers and flag words through
+// CUDA IPC; after the boundary tile bands of step t are computed, the copy
+// engine writes the slab's r outermost rows straight into the neighbours'
+// halo rows (the buffer they read at step t+1) and a stream memory operation
+// bumps the neighbour's flag.  The neighbour's compute stream waits on its own
+// flag before step t+1.  Everything is stream-ordered: no NCCL, no host
+// synchronisation, one host call per step.
+//
+// Hazards (slab boundaries are whole tile bands, band >= r):
+//   RAW  step t+1 of rank k reads halo rows written by the neighbours' step-t
+//        exchange -> cuStreamWaitValue32(flag >= t+1) before step t+1.
+//   WAR  the neighbour's step-(t+1) exchange overwrites rank k's buf[t&1]
+//        halo, read only by rank k's step-t BOUNDARY launch, which completed
+//        before rank k signalled step t (the neighbour waited for that signal
+//        before its step-t+1 boundary launch, which precedes its exchange).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "spider_internal.h"
+
+namespace spd {
+
+typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*WriteValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+struct DriverFns {
+  WaitValueFn wait = nullptr;
+  WriteValueFn write = nullptr;
+  AddrRangeFn range = nullptr;
+};
+
+static const DriverFns& driver() {
+  static DriverFns f;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f.wait = reinterpret_cast<WaitValueFn>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f.write = reinterpret_cast<WriteValueFn>(p);
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      f.range = reinterpret_cast<AddrRangeFn>(p);
+  });
+  return f;
+}
+
+static int cu_err(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return SPD_OK;
+  return set_error(SPD_ECUDA, "%s failed (CUresult %d)", what, (int)r);
+}
+static int rt_err(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SPD_OK;
+  return set_error(SPD_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+}  // namespace spd
+
+struct spd_slab {
+  const spd_plan* plan;
+  spd_grid_desc g;
+  void* buf[2];
+  int band;       // tile band height (rows 2D / planes 3D)
+  int64_t extent; // local rows (2D) / planes (3D)
+  int64_t unit;   // elements per stored row / plane
+  int r;
+  bool has_up, has_dn;
+  void* up_buf[2];
+  void* dn_buf[2];
+  int64_t up_extent, dn_extent;
+  unsigned int* up_flag;  // neighbour's flag word written by us (its "from down" / "from up")
+  unsigned int* dn_flag;
+  unsigned int* my_flags; // [0] from up, [1] from down (written by the neighbours)
+  unsigned int wait_flags;
+  cudaEvent_t boundary_done;
+};
+
+extern "C" {
+
+int spd_ipc_export(const void* ptr, void* handle, int64_t* offset) {
+  using namespace spd;
+  if (!ptr || !handle || !offset) return set_error(SPD_EINVAL, "null argument");
+  const DriverFns& f = driver();
+  if (!f.range) return set_error(SPD_ECUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  int rc = cu_err(f.range(&base, &size, (CUdeviceptr)ptr), "cuMemGetAddressRange");
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  rc = rt_err(cudaIpcGetMemHandle(&h, (void*)base), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = (int64_t)((CUdeviceptr)ptr - base);
+  return SPD_OK;
+}
+
+int spd_ipc_open(const void* handle, int64_t offset, void** ptr, void** base) {
+  using namespace spd;
+  if (!handle || !ptr || !base) return set_error(SPD_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* b = nullptr;
+  int rc = rt_err(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  if (rc) return rc;
+  *base = b;
+  *ptr = (char*)b + offset;
+  return SPD_OK;
+}
+
+int spd_ipc_close(void* base) {
+  using namespace spd;
+  return rt_err(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
+}
+
+int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, void* buf1, void* my_flags,
+                    void* up_buf0, void* up_buf1, const spd_grid_desc* up_g, void* up_flags, void* dn_buf0,
+                    void* dn_buf1, const spd_grid_desc* dn_g, void* dn_flags, spd_slab** out) {
+  using namespace spd;
+  if (!plan || !g || !buf0 || !buf1 || !my_flags || !out) return set_error(SPD_EINVAL, "null argument");
+  if (g->dims == 1) return set_error(SPD_EINVAL, "1D grids have no slab halo");
+  const DriverFns& f = driver();
+  if (!f.wait || !f.write) return set_error(SPD_ECUDA, "stream memory operations unavailable");
+  int32_t info[10];
+  int rc = spd_plan_info(plan, info);
+  if (rc) return rc;
+  spd_slab* s = new spd_slab();
+  s->plan = plan;
+  s->g = *g;
+  s->buf[0] = buf0;
+  s->buf[1] = buf1;
+  s->band = g->dims == 3 ? info[5] : info[6];
+  s->extent = g->dims == 3 ? g->nz : g->ny;
+  s->unit = g->dims == 3 ? g->plane : g->pitch;
+  s->r = g->halo;
+  s->my_flags = (unsigned int*)my_flags;
+  s->has_up = up_buf0 != nullptr;
+  s->has_dn = dn_buf0 != nullptr;
+  if (s->has_up) {
+    if (!up_g || up_g->pitch != g->pitch || up_g->origin != g->origin || (g->dims == 3 && up_g->plane != g->plane) ||
+        !up_flags)
+      return delete s, set_error(SPD_EINVAL, "up neighbour layout differs");
+    s->up_buf[0] = up_buf0;
+    s->up_buf[1] = up_buf1;
+    s->up_extent = up_g->dims == 3 ? up_g->nz : up_g->ny;
+    s->up_flag = (unsigned int*)up_flags + 1;  // its "from down" word
+  }
+  if (s->has_dn) {
+    if (!dn_g || dn_g->pitch != g->pitch || dn_g->origin != g->origin || (g->dims == 3 && dn_g->plane != g->plane) ||
+        !dn_flags)
+      return delete s, set_error(SPD_EINVAL, "down neighbour layout differs");
+    s->dn_buf[0] = dn_buf0;
+    s->dn_buf[1] = dn_buf1;
+    s->dn_extent = dn_g->dims == 3 ? dn_g->nz : dn_g->ny;
+    s->dn_flag = (unsigned int*)dn_flags + 0;  // its "from up" word
+  }
+  if (s->extent < s->r || (s->has_dn && s->extent % s->band != 0))
+    return delete s, set_error(SPD_EINVAL, "slab of %lld rows cannot exchange (band %d)", (long long)s->extent, s->band);
+  // remote-write flush on the waits where the device supports it
+  int dev = 0, can_flush = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&can_flush, cudaDevAttrCanFlushRemoteWrites, dev);
+  s->wait_flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+  rc = rt_err(cudaEventCreateWithFlags(&s->boundary_done, cudaEventDisableTiming), "event");
+  if (rc) return delete s, rc;
+  *out = s;
+  return SPD_OK;
+}
+
+int spd_slab_destroy(spd_slab* s) {
+  if (!s) return SPD_OK;
+  cudaEventDestroy(s->boundary_done);
+  delete s;
+  return SPD_OK;
+}
+
+// Element offset of stored row / plane i (interior index; negative = halo).
+static int64_t unit_start(const spd_grid_desc* g, int64_t unit, int64_t i) {
+  return g->origin - (g->origin % unit) + i * unit;
+}
+
+int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
+  using namespace spd;
+  if (!s) return set_error(SPD_EINVAL, "null slab");
+  const DriverFns& f = driver();
+  cudaStream_t cs = (cudaStream_t)compute_stream, xs = (cudaStream_t)comm_stream;
+  const void* in = s->buf[t & 1];
+  void* out = s->buf[(t + 1) & 1];
+  // 1. this step reads halo rows the neighbours wrote in their step t-1
+  if (t > 0) {
+    if (s->has_up) {
+      int rc = cu_err(f.wait((CUstream)cs, (CUdeviceptr)(s->my_flags + 0), (cuuint32_t)t, s->wait_flags), "wait up");
+      if (rc) return rc;
+    }
+    if (s->has_dn) {
+      int rc = cu_err(f.wait((CUstream)cs, (CUdeviceptr)(s->my_flags + 1), (cuuint32_t)t, s->wait_flags), "wait down");
+      if (rc) return rc;
+    }
+  }
+  // 2. boundary bands (one launch), then the exchange on the comm stream
+  const int64_t last = ((s->extent - 1) / s->band) * s->band;
+  const bool split = last > s->band;
+  int rc = split ? spd_step_edges(s->plan, &s->g, in, out, cs) : spd_step_range(s->plan, &s->g, in, out, 0, s->extent, cs);
+  if (rc) return rc;
+  if (s->has_up || s->has_dn) {
+    rc = rt_err(cudaEventRecord(s->boundary_done, cs), "event record");
+    if (rc) return rc;
+    rc = rt_err(cudaStreamWaitEvent(xs, s->boundary_done, 0), "stream wait event");
+    if (rc) return rc;
+    const size_t bytes = (size_t)s->r * s->unit * 2;
+    const uint16_t* o = (const uint16_t*)out;
+    if (s->has_up) {  // my first r rows -> up neighbour's bottom halo (rows extent_up ..)
+      uint16_t* dst = (uint16_t*)s->up_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, s->up_extent);
+      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, 0), bytes, cudaMemcpyDeviceToDevice, xs),
+                  "peer copy up");
+      if (rc) return rc;
+      rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->up_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
+                  "signal up");
+      if (rc) return rc;
+    }
+    if (s->has_dn) {  // my last r rows -> down neighbour's top halo (rows -r ..)
+      uint16_t* dst = (uint16_t*)s->dn_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, -s->r);
+      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, s->extent - s->r), bytes,
+                                  cudaMemcpyDeviceToDevice, xs),
+                  "peer copy down");
+      if (rc) return rc;
+      rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->dn_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
+                  "signal down");
+      if (rc) return rc;
+    }
+  }
+  // 3. interior bands overlap the exchange
+  if (split) {
+    rc = spd_step_range(s->plan, &s->g, in, out, s->band, last, cs);
+    if (rc) return rc;
+  }
+  return SPD_OK;
+}
+
+}  // extern "C"

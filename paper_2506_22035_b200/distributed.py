@@ -228,3 +228,102 @@ class DeviceSlabOps(SlabOps):
 
 
 __all__ = ["Slab", "decompose", "exchange", "local_exchange", "SlabOps", "SlabDriver", "DeviceSlabOps"]
+
+
+# ---------------------------------------------------------------------------
+# Peer-memory exchange (CUDA IPC + stream memory operations), csrc/peer.cu
+
+
+def _desc_tuple(d) -> tuple:
+    return (d.nz, d.ny, d.nx, d.halo, d.dims, d.pitch, d.plane, d.origin, d.alloc_elems)
+
+
+def _desc_from(t):
+    from ._lib import spd_grid_desc
+
+    d = spd_grid_desc()
+    d.nz, d.ny, d.nx, d.halo, d.dims, d.pitch, d.plane, d.origin, d.alloc_elems = t
+    return d
+
+
+def _ipc_export(t: torch.Tensor):
+    handle = C.create_string_buffer(64)
+    off = C.c_int64(0)
+    check(lib.spd_ipc_export(C.c_void_p(t.data_ptr()), handle, C.byref(off)))
+    return handle.raw, int(off.value)
+
+
+class PeerSlab:
+    """One rank's slab whose halo rows are exchanged through peer memory: the
+    neighbours' grid buffers and flag words are mapped with CUDA IPC, the
+    boundary rows go by copy engine straight into the neighbours' halos and a
+    stream memory operation signals them (spd_slab_step).  One host call per
+    step, no NCCL and no host synchronisation on the data path.  Setup is a
+    collective over `group` (any backend: it only all-gathers the handles).
+
+    The grid must be fully initialised (both buffers, halos included) before
+    construction: the constructor synchronises and barriers, after which the
+    neighbours may write into this rank's halos."""
+
+    def __init__(self, plan: Plan, slab: Slab, grid: DeviceGrid, group=None, compute_stream=None, comm_stream=None):
+        self.plan, self.slab, self.grid = plan, slab, grid
+        dev = grid.bufs[0].device
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.compute_stream = compute_stream or torch.cuda.current_stream(dev)
+        self.comm_stream = comm_stream or torch.cuda.Stream(dev)
+        mine = {
+            "bufs": [_ipc_export(b) for b in grid.bufs],
+            "flags": _ipc_export(self.flags),
+            "desc": _desc_tuple(grid.desc),
+        }
+        torch.cuda.synchronize(dev)
+        world = dist.get_world_size(group)
+        everyone = [None] * world
+        dist.all_gather_object(everyone, mine, group=group)
+        self._bases = []
+        self._descs = {}
+
+        def open_peer(rank):
+            if rank is None:
+                return None, None, None, None
+            info = everyone[rank]
+            ptrs = []
+            for handle, off in info["bufs"] + [info["flags"]]:
+                p, base = C.c_void_p(), C.c_void_p()
+                check(lib.spd_ipc_open(C.create_string_buffer(handle, 64), off, C.byref(p), C.byref(base)))
+                self._bases.append(base)
+                ptrs.append(p)
+            desc = _desc_from(info["desc"])
+            self._descs[rank] = desc
+            return ptrs[0], ptrs[1], desc, ptrs[2]
+
+        ub0, ub1, ud, uf = open_peer(slab.up)
+        db0, db1, dd, df = open_peer(slab.down)
+        h = C.c_void_p()
+        check(lib.spd_slab_create(
+            plan.handle, C.byref(grid.desc), C.c_void_p(grid.bufs[0].data_ptr()), C.c_void_p(grid.bufs[1].data_ptr()),
+            C.c_void_p(self.flags.data_ptr()), ub0, ub1, C.byref(ud) if ud is not None else None, uf,
+            db0, db1, C.byref(dd) if dd is not None else None, df, C.byref(h)))
+        self._h = h
+        self.t = 0
+        dist.barrier(group=group)
+
+    def step(self) -> None:
+        if self.grid.cur != (self.t & 1):
+            raise RuntimeError("the slab grid was stepped outside PeerSlab")
+        check(lib.spd_slab_step(self._h, self.t, C.c_void_p(self.compute_stream.cuda_stream),
+                                C.c_void_p(self.comm_stream.cuda_stream)))
+        self.t += 1
+        self.grid.flip()
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            torch.cuda.synchronize(self.grid.bufs[0].device)
+            lib.spd_slab_destroy(self._h)
+            self._h = None
+            for b in self._bases:
+                lib.spd_ipc_close(b)
+            self._bases = []
+
+
+__all__ += ["PeerSlab"]
