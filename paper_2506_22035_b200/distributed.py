@@ -271,17 +271,24 @@ class PeerSlab:
         self.flags = torch.zeros(2, dtype=torch.int32, device=dev)
         self.compute_stream = compute_stream or torch.cuda.current_stream(dev)
         self.comm_stream = comm_stream or torch.cuda.Stream(dev)
-        mine = {
-            "bufs": [_ipc_export(b) for b in grid.bufs],
-            "flags": _ipc_export(self.flags),
-            "desc": _desc_tuple(grid.desc),
-        }
+        self._bases = []
+        self._descs = {}
+        self._h = None
+        try:
+            mine = {
+                "bufs": [_ipc_export(b) for b in grid.bufs],
+                "flags": _ipc_export(self.flags),
+                "desc": _desc_tuple(grid.desc),
+            }
+        except Exception as exc:  # every rank must reach the all-gather
+            mine = {"error": f"rank {dist.get_rank(group)}: {exc}"}
         torch.cuda.synchronize(dev)
         world = dist.get_world_size(group)
         everyone = [None] * world
         dist.all_gather_object(everyone, mine, group=group)
-        self._bases = []
-        self._descs = {}
+        failed = [e["error"] for e in everyone if "error" in e]
+        if failed:
+            raise RuntimeError("peer-memory exchange unavailable: " + "; ".join(failed))
 
         def open_peer(rank):
             if rank is None:
@@ -297,14 +304,25 @@ class PeerSlab:
             self._descs[rank] = desc
             return ptrs[0], ptrs[1], desc, ptrs[2]
 
-        ub0, ub1, ud, uf = open_peer(slab.up)
-        db0, db1, dd, df = open_peer(slab.down)
-        h = C.c_void_p()
-        check(lib.spd_slab_create(
-            plan.handle, C.byref(grid.desc), C.c_void_p(grid.bufs[0].data_ptr()), C.c_void_p(grid.bufs[1].data_ptr()),
-            C.c_void_p(self.flags.data_ptr()), ub0, ub1, C.byref(ud) if ud is not None else None, uf,
-            db0, db1, C.byref(dd) if dd is not None else None, df, C.byref(h)))
-        self._h = h
+        err = None
+        try:
+            ub0, ub1, ud, uf = open_peer(slab.up)
+            db0, db1, dd, df = open_peer(slab.down)
+            h = C.c_void_p()
+            check(lib.spd_slab_create(
+                plan.handle, C.byref(grid.desc), C.c_void_p(grid.bufs[0].data_ptr()),
+                C.c_void_p(grid.bufs[1].data_ptr()), C.c_void_p(self.flags.data_ptr()), ub0, ub1,
+                C.byref(ud) if ud is not None else None, uf, db0, db1, C.byref(dd) if dd is not None else None, df,
+                C.byref(h)))
+            self._h = h
+        except Exception as exc:  # decided collectively below: all ranks or none
+            err = f"rank {dist.get_rank(group)}: {exc}"
+        errors = [None] * world
+        dist.all_gather_object(errors, err, group=group)
+        errors = [e for e in errors if e]
+        if errors:
+            self.close()
+            raise RuntimeError("peer-memory exchange unavailable: " + "; ".join(errors))
         self.t = 0
         dist.barrier(group=group)
 
@@ -317,13 +335,13 @@ class PeerSlab:
         self.grid.flip()
 
     def close(self) -> None:
+        torch.cuda.synchronize(self.grid.bufs[0].device)
         if getattr(self, "_h", None):
-            torch.cuda.synchronize(self.grid.bufs[0].device)
             lib.spd_slab_destroy(self._h)
             self._h = None
-            for b in self._bases:
-                lib.spd_ipc_close(b)
-            self._bases = []
+        for b in getattr(self, "_bases", []):
+            lib.spd_ipc_close(b)
+        self._bases = []
 
 
 __all__ += ["PeerSlab"]
