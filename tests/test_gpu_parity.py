@@ -448,3 +448,28 @@ def test_step_edges_plus_interior_is_a_full_step(d, shape):
         b.step_range(band, last)
     b.flip()
     assert torch.equal(a.bufs[a.cur], b.bufs[b.cur])
+
+
+@pytest.mark.parametrize("d,r,shape,dtype,parity", [
+    (2, 1, (1000, 4096), "bf16", "even"),
+    (2, 1, (1000, 4096), "fp16", "odd"),
+    (2, 3, (600, 2048), "bf16", "odd"),
+    (3, 1, (40, 48, 256), "bf16", "even"),
+])
+def test_many_tiles_bf16_and_odd_parity(d, r, shape, dtype, parity):
+    """The bf16 and ODD-parity kernel instantiations on grids with many tiles
+    per CTA, against the oracle."""
+    import os
+
+    rng = np.random.default_rng([d, r, 13])
+    c = rng.uniform(0.5, 1.5, (2 * r + 1,) * d)
+    c /= c.sum()
+    k = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
+    plan = get_plan(k, sp.Parity(parity), dtype)
+    dense = quant(rng.uniform(-1, 1, tuple(n + 2 * r for n in shape)), dtype)
+    g = DeviceGrid(plan, shape, r)
+    g.load_dense_f64(torch.from_numpy(dense).cuda())
+    g.run(2)
+    got = g.to_dense_f64().cpu().numpy()
+    want = cnaive.naive_apply(c, d, r, dense, r, 2, threads=os.cpu_count())
+    assert max_rel_error(got, want) < TOL[dtype]
