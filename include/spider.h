@@ -107,9 +107,12 @@ int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype,
 int spd_plan_destroy(spd_plan* plan);
 
 /* Introspection of the packed operands (for the exact-layout tests).
- * info[0..9] = {L, R_in, R_out (per M-tile), S, n_tile, tile_z, tile_y, kchunks,
- * m_tiles, mt_rows}.  The tile has m_tiles M = 128 tiles; M-tile t reuses the
- * MMA schedule with the B rows shifted by t * mt_rows. */
+ * info[0..10] = {L, R_in, R_out (per M-tile), S, n_tile, tile_z, tile_y, kchunks,
+ * m_tiles, mt_rows, cg2}.  The tile has m_tiles M = 128 tiles; M-tile t reuses
+ * the MMA schedule with the B rows shifted by t * mt_rows.  cg2 = 1: a CTA pair
+ * runs one M = 256 MMA per K-block; rank t has its own A/E images (operands
+ * then hold 2 * S records, rank-major) for output rows t * R_out .. and stages
+ * x-half t of the B columns (n_tile per CTA). */
 int spd_plan_info(const spd_plan* plan, int32_t* info);
 /* Host copies of the packed images: a_img[S * 128 * 16] (fp16 bits, logical
  * (s, m, k') order, not the smem swizzle), e_words[S * 128], start_rows[S]. */
@@ -117,7 +120,7 @@ int spd_plan_operands(const spd_plan* plan, uint16_t* a_img, uint32_t* e_words,
                       int32_t* start_rows);
 
 /* Tile geometry tables: in_off[3*R_in] = (dz, dy, dx) of each input image row
- * relative to the tile origin, out_off[3*R_out*m_tiles] likewise for output rows. */
+ * relative to the tile origin, out_off[3*R_out*max(m_tiles, 2*cg2)] likewise for output rows. */
 int spd_plan_geometry(const spd_plan* plan, int32_t* in_off, int32_t* out_off);
 
 /* ---------------------------------------------------------------------------

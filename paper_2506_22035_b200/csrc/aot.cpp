@@ -254,7 +254,19 @@ int build_geometry(int d, int r, Geometry* g) {
     g->n_tile = 32;
     g->tile_x = g->n_tile * L;
     g->mt_rows = (g->tile_z / g->m_tiles) * (g->tile_y + 2 * r);
-    for (int a = 0; a < g->r_out * g->m_tiles; ++a) {
+    // CTA-pair mode (SPD_3D_CG2=1): the same 8z x 8y block, but one
+    // cta_group::2 MMA (M = 256: rank t's TMEM holds M-tile t) per K-block of
+    // all 100 input rows, each CTA staging the B columns of its x-half
+    // (n_tile = 32 chunks per CTA, 64 per pair).
+    {
+      const char* env = getenv("SPD_3D_CG2");
+      if (env && atoi(env) != 0) {
+        g->cg2 = 1;
+        g->m_tiles = 1;
+        g->tile_x = 2 * g->n_tile * L;
+      }
+    }
+    for (int a = 0; a < g->r_out * 2; ++a) {  // two M-tiles (or the two CTAs of a pair)
       g->out_dz[a] = a / g->tile_y;
       g->out_dy[a] = a % g->tile_y;
       g->out_dx[a] = 0;
@@ -297,7 +309,7 @@ int build_geometry(int d, int r, Geometry* g) {
   // an overlapping window whose leading rows carry zero coefficients.
   int rpm = g->rows_per_mma;
   int s = 0;
-  const int rin_mma = rin - (g->m_tiles - 1) * g->mt_rows;  // M-tile 0's input rows
+  const int rin_mma = g->cg2 ? rin : rin - (g->m_tiles - 1) * g->mt_rows;  // M-tile 0's input rows (pair: all)
   for (int b0 = 0; b0 < rin_mma; b0 += rpm) {
     int start = b0 + rpm <= rin_mma ? b0 : rin_mma - rpm;
     g->start_row[s] = start;
@@ -334,16 +346,19 @@ int pack_operands(const Geometry& g, int n_rows, const double* row_values,
                   std::vector<uint32_t>& e_words) {
   const int L = g.L;
   const int segs_per_row = L / 2;  // 4-wide segments in one 2L window
-  a_img.assign((size_t)g.s * 128 * 16, 0);
-  e_words.assign((size_t)g.s * 128, 0);
+  const int ranks = g.cg2 ? 2 : 1;  // CTA pair: rank t's images map output rows t*r_out..
+  a_img.assign((size_t)ranks * g.s * 128 * 16, 0);
+  e_words.assign((size_t)ranks * g.s * 128, 0);
   std::vector<uint8_t> nib((size_t)128 * 8);
+  for (int rk = 0; rk < ranks; ++rk)
   for (int s = 0; s < g.s; ++s) {
+    const size_t si = (size_t)rk * g.s + s;
     std::fill(nib.begin(), nib.end(), (uint8_t)(0 | (1 << 2)));  // empty segment: (0, 1)
     for (int c = 0; c < g.rows_per_mma; ++c) {
       int b = g.start_row[s] + c;
       if (b < g.first_owned[s]) continue;  // owned by the previous MMA
       for (int a = 0; a < g.r_out; ++a) {
-        int kr = kernel_row_index(g, b, a);
+        int kr = kernel_row_index(g, b, a + rk * g.r_out);
         if (kr < 0) continue;
         if (kr >= n_rows) return set_error(SPD_EINVAL, "kernel row %d out of range", kr);
         const double* vals = row_values + (size_t)kr * L * L;
@@ -354,7 +369,7 @@ int pack_operands(const Geometry& g, int n_rows, const double* row_values,
             int kseg = c * 2 * g.kc + sg;  // segment within K=32 (rows padded to kc chunks)
             for (int t = 0; t < 2; ++t) {
               double v = vals[i * L + 2 * sg + t];
-              a_img[((size_t)s * 128 + m) * 16 + 2 * kseg + t] =
+              a_img[(si * 128 + m) * 16 + 2 * kseg + t] =
                   dtype == SPD_DTYPE_BF16 ? f64_to_bf16_bits(v) : f64_to_f16_bits(v);
             }
             const uint8_t* p = meta + (i * segs_per_row + sg) * 2;
@@ -371,7 +386,7 @@ int pack_operands(const Geometry& g, int n_rows, const double* row_values,
           int m = m0 + 8 * m1 + 16 * m2;
           w |= (uint32_t)nib[m * 8 + 4 * k1 + c4] << (16 * m1 + 4 * c4);
         }
-      e_words[(size_t)s * 128 + lane] = w;
+      e_words[si * 128 + lane] = w;
     }
   }
   return SPD_OK;

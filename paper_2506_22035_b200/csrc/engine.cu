@@ -141,6 +141,37 @@ __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
       : "memory");
 }
 
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar, uint32_t rank) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}" ::"r"(bar),
+      "r"(rank)
+      : "memory");
+}
+// CTA-pair sparse MMA (issued by the leader CTA only), M = 256
+__device__ __forceinline__ void mma_sp_ts_elect_cg2(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t e, uint32_t idesc,
+                                                    uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|q, 0xffffffff;\n"
+      "@q tcgen05.mma.sp.cta_group::2.kind::f16 [%0], [%1], %2, [%3], %5, p;\n}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(e), "r"(accum), "r"(idesc));
+}
+__device__ __forceinline__ void tc_commit_mc_elect(uint32_t bar) {
+  asm volatile(
+      "{\n.reg .pred q;\n.reg .b16 mask;\nmov.b16 mask, 3;\nelect.sync _|q, 0xffffffff;\n"
+      "@q tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], mask;\n}" ::"r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_x1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v));
 }
@@ -285,7 +316,7 @@ constexpr int kThreads = 32 * (kPollWarp + 1);
 constexpr int kDQ = 8;                   // poller -> loader ring depth
 constexpr int kNPub = 8;                 // publish ring depth (max tiles per publish batch)
 
-template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0>
+template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
 struct Cfg {
   // fast paths: L = 4 (r = 1) and L = 8 (r = 3); any other even L up to 16 uses
   // the generic producer / epilogue
@@ -311,11 +342,13 @@ struct Cfg {
   static constexpr int STG_BYTES = GEN ? 2 * R_OUT * STG_PITCH + 16 * R_OUT + 16 : 0;
   static constexpr int ACC_COL = 0;
   // MT M-tiles per tile (each M = 128): accumulator stage = MT x NTILE columns
-  static constexpr int ACC_STAGE = MT * NTILE;
+  // (CTA pair: each CTA's accumulator holds the pair's 2 x NTILE columns)
+  static constexpr int ACC_STAGE = MT * NTILE * (CG2 ? 2 : 1);
   static constexpr int E_COL = NACC * ACC_STAGE;
   // E for MMA s at E_COL + 2s: bit 0 of the metadata TMEM address is the
   // sparse_id2 selector, so each MMA's column must be even (odd -> misaligned).
-  static constexpr int A_COL = E_COL + 2 * SPD_MAX_S;
+  static constexpr int S_MMA = (RIN - (MT - 1) * MTR + 4 / KC - 1) / (4 / KC);  // MMAs per M-tile
+  static constexpr int A_COL = E_COL + (2 * S_MMA + 7) / 8 * 8;
   static constexpr int TMEM_COLS = 512;  // host checks A_COL + 8*S <= 512
   static_assert(HALF || NTILE % SEG == 0, "tile width must be whole warp segments");
   // producer work items (input row x warp segment, or row pair) per tile
@@ -411,9 +444,9 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 //   loader --(nat_full: tx bytes)--> producers --(nat_empty)--> loader
 //   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
 //   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
 __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2>;
   constexpr int KC = C::KC;
   constexpr int NQ = C::NQ;
   const Geometry& g = p.g;
@@ -440,6 +473,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  // CTA pair (cluster of 2): both CTAs walk the same tiles; rank 0 issues the MMAs
+  const uint32_t crank = CG2 ? cluster_ctarank() : 0u;
+  const int wid0 = CG2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int wstride = CG2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   if (threadIdx.x == 0) SPD_TRACE(13, 0);
   // let the next step kernel in the stream start its prologue as soon as
   // SMs free up (it still waits for this grid in griddepcontrol.wait)
@@ -447,12 +484,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(bar_full + 8 * s, kProdWarps);
+      mbar_init(bar_full + 8 * s, kProdWarps * (CG2 ? 2 : 1));  // pair: both CTAs' producers
       mbar_init(bar_empty + 8 * s, 1);
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(bar_accf + 8 * a, 1);
-      mbar_init(bar_acce + 8 * a, kEpiWarps);
+      mbar_init(bar_acce + 8 * a, kEpiWarps * (CG2 ? 2 : 1));  // pair: both CTAs' epilogues
     }
     for (int a = 0; a < NNAT; ++a) {
       mbar_init(bar_natf + 8 * a, 1);
@@ -469,9 +506,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "n"(C::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "n"(C::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -485,8 +528,9 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     const int m = warp * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
     for (int s = 0; s < g.s; ++s) {
-      tmem_st_x1(lane_base + C::E_COL + 2 * s, __ldg(p.e_words + s * 128 + m));
-      const uint4* src = reinterpret_cast<const uint4*>(p.a_img + ((size_t)s * 128 + m) * 16);
+      const size_t si = (size_t)crank * g.s + s;  // pair: rank t's own images
+      tmem_st_x1(lane_base + C::E_COL + 2 * s, __ldg(p.e_words + si * 128 + m));
+      const uint4* src = reinterpret_cast<const uint4*>(p.a_img + (si * 128 + m) * 16);
       uint4 a0 = __ldg(src), a1 = __ldg(src + 1);
       uint32_t col = lane_base + C::A_COL + 8 * s;
       tmem_st_x1(col + 0, a0.x);
@@ -502,6 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG2) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
   tc_fence_after();
   // Programmatic dependent launch: everything above (barrier init, TMEM
   // allocation, resident A/E operands) overlaps the previous step kernel's
@@ -562,14 +607,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // with short tiles.
   auto publisher = [&]() {
     int it = 0;
-    for (int gi = blockIdx.x; gi < total;) {
+    for (int gi = wid0; gi < total;) {
       mbar_wait(bar_pubf + 8 * (it % kNPub), (it / kNPub) & 1);
       int n = 1;
-      while (n < kNPub && gi + n * (int)gridDim.x < total &&
+      while (n < kNPub && gi + n * wstride < total &&
              mbar_test(bar_pubf + 8 * ((it + n) % kNPub), ((it + n) / kNPub) & 1))
         ++n;
       if (!(p.dbg & 128)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-      for (int j = 0; j < n; ++j, ++it, gi += gridDim.x) {
+      for (int j = 0; j < n; ++j, ++it, gi += wstride) {
         const TileId id = decode_e(gi, fetch(gi));
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
         mbar_arrive(bar_pube + 8 * (it % kNPub));
@@ -584,14 +629,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     if (lane == 0) {
       const uint32_t box_bytes = (uint32_t)(p.boxw * 2 * g.r_in);
       int it = 0;
-      int2 e_nx = fetch(blockIdx.x);
-      int e_gi = blockIdx.x;
-      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+      int2 e_nx = fetch(wid0);
+      int e_gi = wid0;
+      for (int gi = wid0; gi < total; gi += wstride, ++it) {
         const int ns = it % NNAT;
         const uint32_t nphase = (it / NNAT) & 1;
         const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
-        e_nx = fetch(gi + gridDim.x);
-        e_gi = gi + gridDim.x;
+        e_nx = fetch(gi + wstride);
+        e_gi = gi + wstride;
         const TileId id = decode_e(gi, e_cur);
         const uint32_t dst = nat_s + ns * p.nat_bytes;
         const uint32_t fb = bar_natf + 8 * ns;
@@ -610,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           // where the TMA unit cannot read it)
           const CUtensorMap* map = (id.step & 1) ? &p.tmap[1] : &p.tmap[0];
           mbar_arrive_expect_tx(fb, box_bytes * p.nbox);
-          const int c0 = (int)(p.xoff + id.x0 - 8);
+          const int c0 = (int)(p.xoff + id.x0 - 8) + (int)crank * (NTILE * L);  // pair: x-half of this CTA
           const int c1 = (int)(p.yoff + id.y0 - g.r);
           const int c2 = (int)(p.zoff + id.z0 - g.r);
           for (int k = 0; k < p.nbox; ++k) {
@@ -644,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       constexpr int OFF = R & 1;                  // window-start parity (n*L is even)
       constexpr int NW = (OFF + 2 * L + 1) / 2;  // natural words covering one window
       int it = 0;
-      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+      for (int gi = wid0; gi < total; gi += wstride, ++it) {
         const int stage = it % NSTAGE;
         const uint32_t sphase = (it / NSTAGE) & 1;
         const int ns = it % NNAT;
@@ -739,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       soff[q] = (uint32_t)(b * KC * 128) + (uint32_t)(col / 8) * sbo + (col % 8) * 16;
     }
     int it = 0;
-    for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+    for (int gi = wid0; gi < total; gi += wstride, ++it) {
       const int stage = it % NSTAGE;
       const uint32_t sphase = (it / NSTAGE) & 1;
       const int ns = it % NNAT;
@@ -800,13 +845,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           }
         }
       }
-      fence_proxy_async_smem();
+      if constexpr (CG2) asm volatile("fence.proxy.async;" ::: "memory");  // the pair's MMA reads this B half
+      else fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
         // (releasing the natural stage right after phase 1 was measured
         // slower: deeper TMA prefetch only raised load latency)
         mbar_arrive(bar_nate + 8 * ns);
-        mbar_arrive(bar_full + 8 * stage);
+        if (CG2 && crank != 0) mbar_arrive_cluster(bar_full + 8 * stage, 0);  // the leader issues the MMAs
+        else mbar_arrive(bar_full + 8 * stage);
         if (pw == 0) SPD_TRACE(4, it);
         if (pw == kProdWarps - 1) SPD_TRACE(5, it);
       }
@@ -832,7 +879,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         pend_dep = false;
       };
       int it = 0;
-      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+      for (int gi = wid0; gi < total; gi += wstride, ++it) {
         const TileId id = decode_e(gi, fetch(gi));
         mbar_wait(bar_depe + 8 * (it % kDQ), ((it / kDQ) & 1) ^ 1);
         if (id.step > 0) {
@@ -867,12 +914,13 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     // against ~74 for this form at N = 128 (tools/mma_rate.cu).  The MMA
     // count and start rows are compile-time (start_row(s) = min(s*RPM,
     // RIN-RPM), aot.cpp build_geometry).
-    const uint32_t idesc = idesc_sparse_f16(128, NTILE, std::is_same<T, __nv_bfloat16>::value);
+    const uint32_t idesc = idesc_sparse_f16(CG2 ? 256 : 128, CG2 ? 2 * NTILE : NTILE,
+                                            std::is_same<T, __nv_bfloat16>::value);
     constexpr int RPM = 4 / KC;
     constexpr int RIN_MMA = C::RIN_MMA;
     constexpr int S_CT = (RIN_MMA + RPM - 1) / RPM;
     int it = 0;
-    for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+    for (int gi = wid0; gi < total && !(CG2 && crank != 0); gi += wstride, ++it) {
       const int stage = it % NSTAGE;
       const uint32_t sphase = (it / NSTAGE) & 1;
       const int acc = it % NACC;
@@ -892,12 +940,20 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           const int start = (s * RPM + RPM <= RIN_MMA ? s * RPM : RIN_MMA - RPM) + mt * MTR;
           // descriptor start address field is addr >> 4
           const uint64_t bdesc = bdesc0 + (uint64_t)((start * KC * 128) >> 4);
-          mma_sp_ts_elect(dcol + mt * NTILE, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc,
-                          s > 0 ? 1u : 0u);
+          if constexpr (CG2)
+            mma_sp_ts_elect_cg2(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
+          else
+            mma_sp_ts_elect(dcol + mt * NTILE, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc,
+                            s > 0 ? 1u : 0u);
         }
       }
-      tc_commit_elect(bar_empty + 8 * stage);
-      tc_commit_elect(bar_accf + 8 * acc);
+      if constexpr (CG2) {  // both CTAs' B stage and accumulator barriers
+        tc_commit_mc_elect(bar_empty + 8 * stage);
+        tc_commit_mc_elect(bar_accf + 8 * acc);
+      } else {
+        tc_commit_elect(bar_empty + 8 * stage);
+        tc_commit_elect(bar_accf + 8 * acc);
+      }
       __syncwarp();
     }
   } else {
@@ -929,14 +985,14 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
       int bt = 0;
       int it = 0;
-      int2 e_nx = fetch(blockIdx.x);
-      int e_gi = blockIdx.x;
-      for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+      int2 e_nx = fetch(wid0);
+      int e_gi = wid0;
+      for (int gi = wid0; gi < total; gi += wstride, ++it) {
         const int acc = it % NACC;
         const uint32_t aphase = (it / NACC) & 1;
         const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
-        e_nx = fetch(gi + gridDim.x);
-        e_gi = gi + gridDim.x;
+        e_nx = fetch(gi + wstride);
+        e_gi = gi + wstride;
         const TileId id = decode_e(gi, e_cur);
         T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
         mbar_wait(bar_accf + 8 * acc, aphase);
@@ -953,7 +1009,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           if (cb == NB - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
+            if (lane == 0) {
+            if (CG2 && crank != 0) mbar_arrive_cluster(bar_acce + 8 * acc, 0);
+            else mbar_arrive(bar_acce + 8 * acc);
+          }
           }
           const uint32_t sb = stg_s + (bt & 1) * (C::R_OUT * C::STG_PITCH);
 #pragma unroll
@@ -1016,20 +1075,20 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     int odz[MT], ody[MT], odx[MT];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
-      odz[mt] = g.out_dz[alpha + mt * C::R_OUT];
-      ody[mt] = g.out_dy[alpha + mt * C::R_OUT];
-      odx[mt] = g.out_dx[alpha + mt * C::R_OUT];
+      odz[mt] = g.out_dz[alpha + (mt + (int)crank) * C::R_OUT];
+      ody[mt] = g.out_dy[alpha + (mt + (int)crank) * C::R_OUT];
+      odx[mt] = g.out_dx[alpha + (mt + (int)crank) * C::R_OUT];
     }
     int it = 0;
-    int2 e_nx = fetch(blockIdx.x);
-    int e_gi = blockIdx.x;
-    for (int gi = blockIdx.x; gi < total; gi += gridDim.x, ++it) {
+    int2 e_nx = fetch(wid0);
+    int e_gi = wid0;
+    for (int gi = wid0; gi < total; gi += wstride, ++it) {
       if (kEpiGroups > 1 && (it % kEpiGroups) != grp) continue;
       const int acc = it % NACC;
       const uint32_t aphase = (it / NACC) & 1;
       const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
-      e_nx = fetch(gi + gridDim.x);
-      e_gi = gi + gridDim.x;
+      e_nx = fetch(gi + wstride);
+      e_gi = gi + wstride;
       const TileId id = decode_e(gi, e_cur);
       T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
       bool row_ok[MT];
@@ -1055,7 +1114,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       // pairs: the two butterflies are independent shuffle chains the
       // scheduler interleaves (the epilogue is latency-bound), and the TMEM
       // load of the next batch is in flight while the current one is packed.
-      constexpr int NB = NTILE / 32;  // batches per M-tile
+      constexpr int NB = C::ACC_STAGE / MT / 32;  // batches per M-tile (pair: both x-halves)
       constexpr int TB = MT * NB;     // batches per tile (batch bi: M-tile bi / NB, column batch bi % NB)
       static_assert(TB % 2 == 0, "epilogue processes batch pairs");
       constexpr int PPD = 16 / L;  // packed words (chunk pairs) per destination lane
@@ -1128,7 +1187,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           // every accumulator column is in registers: free the stage
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
+          if (lane == 0) {
+            if (CG2 && crank != 0) mbar_arrive_cluster(bar_acce + 8 * acc, 0);
+            else mbar_arrive(bar_acce + 8 * acc);
+          }
         }
 #pragma unroll
         for (int b = 1; b < L; b <<= 1) {
@@ -1176,9 +1238,13 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) SPD_TRACE(15, 0);
+  if constexpr (CG2) cluster_sync_all();  // the peer's MMAs into this TMEM are complete
   if (warp == kMmaWarp) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+    if constexpr (CG2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TMEM_COLS));
   }
 }
 
@@ -1381,10 +1447,11 @@ static int plan_counters(const spd_plan* cplan, int n, cudaStream_t st, unsigned
   return cuda_err(cudaMemsetAsync(plan->d_counters, 0, sizeof(unsigned int) * n, st), "counter reset");
 }
 
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR>;
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2>;
+  if (CG2 != (plan->g.cg2 != 0)) return set_error(SPD_EUNSUPPORTED, "CTA-pair geometry mismatch");
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
   {  // the MMA issuer's compile-time schedule must be the plan's
     constexpr int RPM = 4 / C::KC;
@@ -1415,14 +1482,24 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     configured_smem = 232448;
   }
   if (sp.n_tiles <= 0) return SPD_OK;
-  const int64_t work = (int64_t)sp.n_tiles * sp.steps;
+  const int64_t work = (int64_t)sp.n_tiles * sp.steps * (CG2 ? 2 : 1);
   int grid = work < plan->sms ? (int)work : plan->sms;
+  if (CG2) grid &= ~1;  // whole CTA pairs
+  if (CG2 && sp.steps > 1) return set_error(SPD_EUNSUPPORTED, "persistent launch not supported in CTA-pair mode");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  unsigned int nattr = 1;
+  if (CG2) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    nattr = 2;
+  }
   if (sp.steps > 1) {
     attr[0].id = cudaLaunchAttributeCooperative;  // co-residency: cross-step waits need every CTA running
     attr[0].val.cooperative = 1;
@@ -1432,7 +1509,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     attr[0].val.programmaticStreamSerializationAllowed = pdl_env ? 0 : 1;
   }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = nattr;
   return cuda_err(cudaLaunchKernelEx(&cfg, kern, sp), "spider_step_kernel launch");
 }
 
@@ -1446,6 +1523,8 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
     return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.cg2)
+    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, 3, 100, 1, 0, true>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 22>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16>(plan, sp, st);
   // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
@@ -1749,6 +1828,7 @@ int spd_plan_info(const spd_plan* plan, int32_t* info) {
   info[7] = g.kc;
   info[8] = g.m_tiles;
   info[9] = g.mt_rows;
+  info[10] = g.cg2;
   return SPD_OK;
 }
 
@@ -1769,7 +1849,7 @@ int spd_plan_geometry(const spd_plan* plan, int32_t* in_off, int32_t* out_off) {
     in_off[3 * b + 1] = g.in_dy[b];
     in_off[3 * b + 2] = g.in_dx[b];
   }
-  for (int a = 0; out_off && a < g.r_out * g.m_tiles; ++a) {
+  for (int a = 0; out_off && a < g.r_out * (g.cg2 ? 2 : g.m_tiles); ++a) {
     out_off[3 * a] = g.out_dz[a];
     out_off[3 * a + 1] = g.out_dy[a];
     out_off[3 * a + 2] = g.out_dx[a];

@@ -128,7 +128,7 @@ int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, vo
   if (g->dims == 1) return set_error(SPD_EINVAL, "1D grids have no slab halo");
   const DriverFns& f = driver();
   if (!f.wait || !f.write) return set_error(SPD_ECUDA, "stream memory operations unavailable");
-  int32_t info[10];
+  int32_t info[16];  // spd_plan_info writes 11 entries
   int rc = spd_plan_info(plan, info);
   if (rc) return rc;
   spd_slab* s = new spd_slab();

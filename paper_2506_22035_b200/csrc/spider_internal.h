@@ -11,7 +11,7 @@
 #define SPD_ABI_VERSION 1
 #define SPD_MAX_RIN 128
 #define SPD_MAX_ROUT 64
-#define SPD_MAX_S 24
+#define SPD_MAX_S 32
 
 namespace spd {
 
@@ -41,6 +41,8 @@ struct Geometry {
   int r_out;         // output rows per M-tile (128/L)
   int m_tiles;       // M = 128 tiles per tile (3D: 2, sharing one input block)
   int mt_rows;       // input-row offset between consecutive M-tiles
+  int cg2;           // 3D CTA-pair mode: one M = 256 tcgen05.mma.sp.cta_group::2 per K-block;
+                     // CTA rank t holds output rows t*r_out.. (its own A/E images) and x-half t of B
   int r_in;          // input image rows per tile
   int s;             // MMAs per tile
   int n_tile;        // x-chunks per tile (MMA N)

@@ -49,6 +49,7 @@ class PlanInfo:
     kchunks: int
     m_tiles: int = 1  # M = 128 tiles per tile (3D: 2, sharing one input block)
     mt_rows: int = 0  # input-row shift of M-tile t's MMA schedule: t * mt_rows
+    cg2: int = 0      # CTA-pair mode (3D): rank t owns M-tile t and its own A/E images
 
 
 class Plan:
@@ -89,15 +90,17 @@ class Plan:
             pass
 
     def info(self) -> PlanInfo:
-        buf = np.zeros(10, dtype=np.int32)
+        buf = np.zeros(11, dtype=np.int32)
         check(lib.spd_plan_info(self._h, i32ptr(buf)))
         return PlanInfo(*[int(v) for v in buf])
 
     def operands(self):
-        """(a_img [S,128,16] uint16, e_words [S,128] uint32, start_rows [S])."""
+        """(a_img [R*S,128,16] uint16, e_words [R*S,128] uint32, start_rows [S]);
+        R = 2 in CTA-pair mode (rank-major), else 1."""
         inf = self.info()
-        a = np.zeros((inf.mmas_per_tile, 128, 16), dtype=np.uint16)
-        e = np.zeros((inf.mmas_per_tile, 128), dtype=np.uint32)
+        ranks = 2 if inf.cg2 else 1
+        a = np.zeros((ranks * inf.mmas_per_tile, 128, 16), dtype=np.uint16)
+        e = np.zeros((ranks * inf.mmas_per_tile, 128), dtype=np.uint32)
         s = np.zeros(inf.mmas_per_tile, dtype=np.int32)
         check(lib.spd_plan_operands(self._h, u16ptr(a), u32ptr(e), i32ptr(s)))
         return a, e, s
@@ -106,7 +109,7 @@ class Plan:
         """(in_off [R_in,3], out_off [R_out*m_tiles,3]) tile row offsets (dz, dy, dx)."""
         inf = self.info()
         a = np.zeros((inf.r_in, 3), dtype=np.int32)
-        b = np.zeros((inf.r_out * inf.m_tiles, 3), dtype=np.int32)
+        b = np.zeros((inf.r_out * (2 if inf.cg2 else inf.m_tiles), 3), dtype=np.int32)
         check(lib.spd_plan_geometry(self._h, i32ptr(a), i32ptr(b)))
         return a, b
 

@@ -42,7 +42,7 @@ def tile_model(plan, dense, halo):
     kern = plan.kernel
     r = kern.r
     inf = plan.info()
-    L, n_tile = inf.L, inf.n_tile
+    L, n_tile = inf.L, inf.n_tile * (2 if inf.cg2 else 1)  # a CTA pair spans both x-halves
     a_img, e_words, starts = plan.operands()
     in_off, out_off = plan.geometry()
     perm = sp.input_row_permutation(L, plan.parity).mapping
@@ -63,12 +63,13 @@ def tile_model(plan, dense, halo):
     out = {}
     # M-tile t runs the same MMA schedule (same A/E) on B rows shifted by
     # t * mt_rows and produces output rows t * r_out ..
-    for t in range(inf.m_tiles):
+    # CTA-pair mode: rank t runs every K-block with its own A images
+    for t in range(2 if inf.cg2 else inf.m_tiles):
         D = np.zeros((128, n_tile))
         for s in range(inf.mmas_per_tile):
-            b0 = starts[s] + t * inf.mt_rows
+            b0 = starts[s] + (0 if inf.cg2 else t * inf.mt_rows)
             Bs = Bimg[b0 : b0 + rpm].transpose(0, 2, 1).reshape(32, n_tile)
-            D += A[s] @ Bs
+            D += A[t * inf.mmas_per_tile + s if inf.cg2 else s] @ Bs
         for a in range(inf.r_out):
             dz, dy, dx = out_off[a + t * inf.r_out]
             for i in range(L):
@@ -118,7 +119,7 @@ def test_tile_model_matches_oracle(shape, d, r, parity):
     L = inf.L
     in_off, out_off = plan.geometry()
     if d == 3:
-        shape3 = (inf.tile_z, inf.tile_y, inf.n_tile * L)
+        shape3 = (inf.tile_z, inf.tile_y, inf.n_tile * L * (2 if inf.cg2 else 1))
     elif d == 2:
         shape3 = (inf.tile_y, inf.n_tile * L)
     else:

@@ -473,3 +473,28 @@ def test_many_tiles_bf16_and_odd_parity(d, r, shape, dtype, parity):
     got = g.to_dense_f64().cpu().numpy()
     want = cnaive.naive_apply(c, d, r, dense, r, 2, threads=os.cpu_count())
     assert max_rel_error(got, want) < TOL[dtype]
+
+
+@pytest.mark.parametrize("shape", [(16, 16, 512), (40, 48, 256), (64, 64, 600)])
+def test_cta_pair_3d_bit_identical(monkeypatch, shape):
+    """3D CTA-pair mode (SPD_3D_CG2=1: one M = 256 tcgen05.mma.sp.cta_group::2
+    per K-block, each CTA staging one x-half of B and holding one M-tile's
+    A/E) gives the same bits as the default two-M-tile kernel."""
+    from paper_2506_22035_b200.engine import Plan
+
+    rng = np.random.default_rng(3)
+    c = rng.uniform(0.5, 1.5, (3, 3, 3))
+    c /= c.sum()
+    k = sp.make_kernel_3d("box", 1, c)
+    torch.manual_seed(0)
+    dense = torch.rand(tuple(n + 2 for n in shape), dtype=torch.float64, device="cuda") - 0.5
+    outs = []
+    for cg2 in ("0", "1"):
+        monkeypatch.setenv("SPD_3D_CG2", cg2)
+        plan = Plan(k, sp.Parity.EVEN, "fp16")
+        assert plan.info().cg2 == int(cg2)
+        g = DeviceGrid(plan, shape, 1)
+        g.load_dense_f64(dense)
+        g.run(3)
+        outs.append(g.to_dense_f64())
+    assert torch.equal(outs[0], outs[1])
