@@ -3,19 +3,24 @@
 // behind the C ABI (include/spider.h).
 //
 // One launch = one Jacobi step (pipeline.py:247-261 / core.py:176-181) over a
-// tile range.  Persistent, warp-specialised CTA (one per SM):
-//   warps 0-3  epilogue : TMEM -> registers -> fp16 -> quad/octet transpose ->
-//                         coalesced 16-byte global stores
-//   warps 4-11 producer : LDG.128 of the natural input rows -> warp shuffles
-//                         -> PRMT byte permutes that apply the reference's
-//                         input-row involution (transform.py:130-139) and the
-//                         2L-window expansion (pipeline.py:176-186, 251-252)
-//                         -> STS.128 straight into the UMMA K-major B image.
-//                         The swap costs no extra pass: it is folded into the
-//                         register->smem write.
-//   warp 12    MMA      : one thread issues S tcgen05.mma.sp per tile with the
+// tile range (or, SPD_RUN_PERSISTENT, all steps in L2-wavefront order).
+// Persistent, warp-specialised CTA (one per SM, 16 warps):
+//   warps 0-3  epilogue : TMEM -> registers -> fp16 -> xor-butterfly transpose
+//                         inside each L-lane group -> 256-bit stores, each
+//                         instruction writing whole 128-byte lines
+//   warps 4-11 producer : LDS.128 of the TMA-staged natural input rows -> warp
+//                         shuffles -> PRMT byte permutes that apply the
+//                         reference's input-row involution (transform.py:
+//                         130-139) and the 2L-window expansion (pipeline.py:
+//                         176-186, 251-252) -> STS.128 straight into the UMMA
+//                         K-major B image.  The swap costs no extra pass: it is
+//                         folded into the register->smem write.
+//   warp 12    MMA      : the converged warp runs a compile-time MMA schedule,
+//                         one elected lane issues tcgen05.mma.sp with the
 //                         compressed kernel (A) and metadata (E) resident in
 //                         TMEM for the whole launch.
+//   warp 13    loader   : cp.async.bulk.tensor boxes of the halo-padded block.
+//   warps 14-15         : publisher / dependency poller (persistent launches).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
