@@ -163,6 +163,15 @@ int spd_run_ex(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
 int spd_step_edges(const spd_plan* plan, const spd_grid_desc* g, const void* in,
                    void* out, void* stream);
 
+/* One step over the tile bands listed in `order` (n_pairs int2 entries
+ * {0, band}, in execution order).  publish != 0: every finished tile bumps
+ * band_done[band] after a system-scope release, so a copy engine waiting on
+ * the counters (cuStreamWaitValue32) can move a band's rows while the rest of
+ * the step is still running.  2D / 3D only. */
+int spd_step_ordered(const spd_plan* plan, const spd_grid_desc* g, const void* in,
+                     void* out, const void* order, int n_pairs,
+                     unsigned int* band_done, int publish, void* stream);
+
 /* One step restricted to output rows [y_begin, y_end) (2D) or planes
  * [z_begin, z_end) (3D) — used by the slab driver to compute the boundary
  * bands before the halo exchange and the interior after. */

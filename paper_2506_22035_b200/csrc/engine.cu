@@ -272,6 +272,9 @@ struct StepParams {
   // few wavefronts earlier, still resident in L2 (temporal blocking through
   // the 126 MB L2).
   int sweep, lag, total;     // total = pairs * per_band work items
+  int use_order;             // steps == 1 with a host-given band order (slab step: edge bands first)
+  int publish;               // steps == 1: publish finished tiles to band_done (system scope) for a
+                             // copy engine waiting on them (peer exchange inside one launch)
   const int2* order;         // [pairs] (step, band) in execution order (host-built)
   int64_t pitch, plane, origin;
   int64_t nx;                // x extent (interior)
@@ -569,7 +572,9 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // smaller work indices, so with all CTAs co-resident (cooperative launch)
   // the smallest unfinished tile can always proceed.  Static round-robin
   // over CTAs.
-  const int total = p.steps > 1 ? p.total : p.n_tiles;
+  const bool ordered = p.steps > 1 || p.use_order;
+  const bool publishing = p.steps > 1 || p.publish;
+  const int total = ordered ? p.total : p.n_tiles;
   struct TileId {
     int step, band;
     int64_t z0, y0, x0;
@@ -578,13 +583,13 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // next tile is issued before this tile's work), so the dependent global
   // load never sits on a role's critical path.
   auto fetch = [&](int gi) -> int2 {
-    if (p.steps == 1 || gi >= total) return make_int2(0, 0);
+    if (!ordered || gi >= total) return make_int2(0, 0);
     return __ldg(p.order + gi / p.per_band);
   };
   auto decode_e = [&](int gi, int2 e) {
     TileId id;
     int t;
-    if (p.steps == 1) {
+    if (!ordered) {
       id.step = 0;
       t = p.reverse ? p.n_tiles - 1 - gi : gi;
     } else {
@@ -610,7 +615,24 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // CTA-scope mbarrier release/acquire) followed by relaxed increments: the
   // fence waits for the store drain, so one fence per tile cannot keep up
   // with short tiles.
+  // single-step publishing (slab step): only the two edge bands' tiles
+  auto pub_tile = [&](const TileId& id) {
+    return p.steps > 1 || id.band == 0 || id.band == p.n_bands - 1;
+  };
   auto publisher = [&]() {
+    if (p.steps == 1) {
+      int pit = 0;
+      for (int gi = wid0; gi < total; gi += wstride) {
+        const TileId id = decode_e(gi, fetch(gi));
+        if (!pub_tile(id)) continue;
+        mbar_wait(bar_pubf + 8 * (pit % kNPub), (pit / kNPub) & 1);
+        asm volatile("fence.acq_rel.sys;" ::: "memory");  // observed by a copy engine
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+        mbar_arrive(bar_pube + 8 * (pit % kNPub));
+        ++pit;
+      }
+      return;
+    }
     int it = 0;
     for (int gi = wid0; gi < total;) {
       mbar_wait(bar_pubf + 8 * (it % kNPub), (it / kNPub) & 1);
@@ -865,7 +887,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
     }
   } else if (warp == kPubWarp) {
-    if (p.steps > 1 && lane == 0) publisher();
+    if (publishing && lane == 0) publisher();
   } else if (warp == kPollWarp) {
     // ===================== dependency poller (persistent launches) =========
     // Tiles whose dependencies are already met are released in batches of
@@ -990,6 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
       int bt = 0;
       int it = 0;
+      int pit = 0;  // published tiles (publish ring index)
       int2 e_nx = fetch(wid0);
       int e_gi = wid0;
       for (int gi = wid0; gi < total; gi += wstride, ++it) {
@@ -1058,14 +1081,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           }
           if (cb + 1 < NB) tmem_wait_ld();
         }
-        if (p.steps > 1) {
+        if (publishing && pub_tile(id)) {
           // hand the tile to the publisher warp (release at CTA scope after
           // the warp's stores); the gpu-scope release happens off this path
-          const int ps = it % kNPub;
-          mbar_wait(bar_pube + 8 * ps, ((it / kNPub) & 1) ^ 1);
+          const int ps = pit % kNPub;
+          mbar_wait(bar_pube + 8 * ps, ((pit / kNPub) & 1) ^ 1);
           if (p.dbg & 256) __threadfence();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
+          ++pit;
         }
       }
      }
@@ -1085,6 +1109,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       odx[mt] = g.out_dx[alpha + (mt + (int)crank) * C::R_OUT];
     }
     int it = 0;
+    int pit = 0;  // published tiles (publish ring index)
     int2 e_nx = fetch(wid0);
     int e_gi = wid0;
     for (int gi = wid0; gi < total; gi += wstride, ++it) {
@@ -1227,14 +1252,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         if (cb1 + 1 < TB) tmem_wait_ld();
       }
       if (warp == 0 && lane == 0) SPD_TRACE(9, it);
-      if (p.steps > 1) {
+      if (publishing && pub_tile(id)) {
         // hand the tile to the publisher warp (release at CTA scope after
         // the warp's stores); the gpu-scope release happens off this path
-        const int ps = it % kNPub;
-        mbar_wait(bar_pube + 8 * ps, ((it / kNPub) & 1) ^ 1);
+        const int ps = pit % kNPub;
+        mbar_wait(bar_pube + 8 * ps, ((pit / kNPub) & 1) ^ 1);
         if (p.dbg & 256) __threadfence();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
+        ++pit;
       }
     }
     }
@@ -1937,6 +1963,27 @@ int spd_step_edges(const spd_plan* plan, const spd_grid_desc* gd, const void* in
     sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
     sp.n_bands = 2;
   }
+  return dispatch(plan, sp, (cudaStream_t)stream);
+}
+
+int spd_step_ordered(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, const void* order,
+                     int n_pairs, unsigned int* band_done, int publish, void* stream) {
+  using namespace spd;
+  int rc = check_desc(plan, gd);
+  if (rc) return rc;
+  if (plan->d == 1) return set_error(SPD_EINVAL, "band orders are defined for 2D / 3D grids");
+  if (plan->g.cg2) return set_error(SPD_EUNSUPPORTED, "ordered launch not supported in CTA-pair mode");
+  const int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
+  StepParams sp;
+  rc = fill_step_params(plan, gd, in, out, 0, extent, 1, sp);
+  if (rc) return rc;
+  if (!order || n_pairs < 1 || n_pairs > sp.n_bands) return set_error(SPD_EINVAL, "bad band order (%d pairs)", n_pairs);
+  if (publish && !band_done) return set_error(SPD_EINVAL, "publishing needs band counters");
+  sp.use_order = 1;
+  sp.order = (const int2*)order;
+  sp.total = n_pairs * sp.per_band;
+  sp.publish = publish ? 1 : 0;
+  sp.band_done = band_done;
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
 

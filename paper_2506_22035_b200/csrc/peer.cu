@@ -18,7 +18,9 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "spider_internal.h"
 
@@ -81,6 +83,12 @@ struct spd_slab {
   unsigned int* my_flags; // [0] from up, [1] from down (written by the neighbours)
   unsigned int wait_flags;
   cudaEvent_t boundary_done;
+  // one launch per step: edge bands first, published per band; the copy
+  // engine waits on the edge bands' counters instead of a kernel boundary
+  int n_bands, per_band;
+  int2* order = nullptr;             // device: 2 x n_bands {0, band}: edge bands first, then the
+                                     // interior forward (even steps) / backward (odd steps, L2 reuse)
+  unsigned int* band_done = nullptr; // device: cumulative finished tiles per band
 };
 
 extern "C" {
@@ -170,6 +178,25 @@ int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, vo
   s->wait_flags = CU_STREAM_WAIT_VALUE_GEQ | (can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
   rc = rt_err(cudaEventCreateWithFlags(&s->boundary_done, cudaEventDisableTiming), "event");
   if (rc) return delete s, rc;
+  {
+    const int tile_x = info[4] * info[0];  // n_tile * L (single-CTA geometry)
+    const int64_t tiles_x = (g->nx + tile_x - 1) / tile_x;
+    const int64_t tiles_y = g->dims == 3 ? (g->ny + info[6] - 1) / info[6] : 1;
+    s->per_band = (int)(tiles_x * tiles_y);
+    s->n_bands = (int)((s->extent + s->band - 1) / s->band);
+    std::vector<int2> ord;
+    for (int dir = 0; dir < 2; ++dir) {
+      const int first = dir ? s->n_bands - 1 : 0, second = dir ? 0 : s->n_bands - 1;
+      ord.push_back(make_int2(0, first));
+      if (s->n_bands > 1) ord.push_back(make_int2(0, second));
+      for (int k = 1; k < s->n_bands - 1; ++k) ord.push_back(make_int2(0, dir ? s->n_bands - 1 - k : k));
+    }
+    rc = rt_err(cudaMalloc(&s->order, sizeof(int2) * ord.size()), "order alloc");
+    if (!rc) rc = rt_err(cudaMemcpy(s->order, ord.data(), sizeof(int2) * ord.size(), cudaMemcpyHostToDevice), "order");
+    if (!rc) rc = rt_err(cudaMalloc(&s->band_done, sizeof(unsigned int) * s->n_bands), "counter alloc");
+    if (!rc) rc = rt_err(cudaMemset(s->band_done, 0, sizeof(unsigned int) * s->n_bands), "counter reset");
+    if (rc) return spd_slab_destroy(s), rc;
+  }
   *out = s;
   return SPD_OK;
 }
@@ -177,6 +204,8 @@ int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, vo
 int spd_slab_destroy(spd_slab* s) {
   if (!s) return SPD_OK;
   cudaEventDestroy(s->boundary_done);
+  if (s->order) cudaFree(s->order);
+  if (s->band_done) cudaFree(s->band_done);
   delete s;
   return SPD_OK;
 }
@@ -204,7 +233,43 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
       if (rc) return rc;
     }
   }
-  // 2. boundary bands (one launch), then the exchange on the comm stream
+  // 2a. one launch, edge bands first and published per band; the copy engine
+  //     starts on the edge rows while the interior is still being computed
+  static const char* two_launch = getenv("SPD_SLAB_TWO_LAUNCH");
+  if ((s->has_up || s->has_dn) && !two_launch) {
+    int rc0 = spd_step_ordered(s->plan, &s->g, in, out, s->order + (t & 1) * s->n_bands, s->n_bands, s->band_done, 1, cs);
+    if (rc0) return rc0;
+    const cuuint32_t target = (cuuint32_t)((int64_t)(t + 1) * s->per_band);
+    const size_t bytes = (size_t)s->r * s->unit * 2;
+    const uint16_t* o = (const uint16_t*)out;
+    if (s->has_up) {
+      int rc = cu_err(f.wait((CUstream)xs, (CUdeviceptr)(s->band_done + 0), target, CU_STREAM_WAIT_VALUE_GEQ),
+                      "wait top band");
+      if (rc) return rc;
+      uint16_t* dst = (uint16_t*)s->up_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, s->up_extent);
+      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, 0), bytes, cudaMemcpyDeviceToDevice, xs),
+                  "peer copy up");
+      if (rc) return rc;
+      rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->up_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
+                  "signal up");
+      if (rc) return rc;
+    }
+    if (s->has_dn) {
+      int rc = cu_err(f.wait((CUstream)xs, (CUdeviceptr)(s->band_done + s->n_bands - 1), target, CU_STREAM_WAIT_VALUE_GEQ),
+                      "wait bottom band");
+      if (rc) return rc;
+      uint16_t* dst = (uint16_t*)s->dn_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, -s->r);
+      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, s->extent - s->r), bytes,
+                                  cudaMemcpyDeviceToDevice, xs),
+                  "peer copy down");
+      if (rc) return rc;
+      rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->dn_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
+                  "signal down");
+      if (rc) return rc;
+    }
+    return SPD_OK;
+  }
+  // 2b. boundary bands (one launch), then the exchange on the comm stream
   const int64_t last = ((s->extent - 1) / s->band) * s->band;
   const bool split = last > s->band;
   int rc = split ? spd_step_edges(s->plan, &s->g, in, out, cs) : spd_step_range(s->plan, &s->g, in, out, 0, s->extent, cs);
