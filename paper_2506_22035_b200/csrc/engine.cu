@@ -259,6 +259,8 @@ struct StepParams {
   CUtensorMap tmap[2];       // buf[0] / buf[1] as 2D / 3D tensors (tensor-TMA mode)
   Geometry g;
   int use_tmap;              // 1: tensor-TMA boxes, 0: 1D bulk copies per row
+  int rowmajor;              // 2D generic radii: ONE 3D-view TMA box per tile lands the block as
+                             // contiguous rows [row][nbox*boxw] (no box boundaries inside a row)
   int nbox, boxw, box_slot;  // natural-stage layout: [box][row][boxw] elements
   int nat_bytes;             // bytes per natural stage
   int xoff, yoff, zoff;      // stored coordinates of interior (0, 0, 0)
@@ -685,9 +687,13 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           const int c0 = (int)(p.xoff + id.x0 - 8) + (int)crank * (NTILE * L);  // pair: x-half of this CTA
           const int c1 = (int)(p.yoff + id.y0 - g.r);
           const int c2 = (int)(p.zoff + id.z0 - g.r);
-          for (int k = 0; k < p.nbox; ++k) {
-            if (g.d == 3) tma_load_3d(dst + k * p.box_slot, map, c0 + k * p.boxw, c1, c2, fb);
-            else tma_load_2d(dst + k * p.box_slot, map, c0 + k * p.boxw, c1, fb);
+          if (p.rowmajor) {
+            tma_load_3d(dst, map, c0, 0, c1, fb);  // view (x, box, row): rows land contiguous
+          } else {
+            for (int k = 0; k < p.nbox; ++k) {
+              if (g.d == 3) tma_load_3d(dst + k * p.box_slot, map, c0 + k * p.boxw, c1, c2, fb);
+              else tma_load_2d(dst + k * p.box_slot, map, c0 + k * p.boxw, c1, fb);
+            }
           }
         } else {
           mbar_arrive_expect_tx(fb, (uint32_t)(g.r_in * C::ROW_BYTES));
@@ -733,13 +739,35 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           const int n = sg * 32 + lane;
           const int s_al = n * L - R + 8 - OFF;
           uint32_t w[NW];
+          if (p.rowmajor) {
+            // contiguous rows [row][NBOX*BOXW]
+            const uint32_t rb = nbase + (uint32_t)(b * C::NBOX * C::BOXW + s_al) * 2;
+            if constexpr (L == 16) {
+              // window start 16n: 32-B aligned, 128-bit loads (2-way instead
+              // of 8-way bank conflicts for 32-bit loads at a 32-B lane stride)
 #pragma unroll
-          for (int k = 0; k < NW; ++k) {
-            const int e = s_al + 2 * k;
-            // tensor-TMA stage: [box][row][BOXW]; 1D bulk stage: [row][ROW_ELEMS]
-            const int kb = p.use_tmap ? e / C::BOXW : 0;
-            const int bw = p.use_tmap ? C::BOXW : C::ROW_ELEMS;
-            w[k] = lds_u32(nbase + kb * p.box_slot + (b * bw + e - kb * bw) * 2);
+              for (int k = 0; k + 4 <= NW; k += 4) {
+                const uint4 v = lds_v4(rb + 4 * k);
+                w[k] = v.x;
+                w[k + 1] = v.y;
+                w[k + 2] = v.z;
+                w[k + 3] = v.w;
+              }
+#pragma unroll
+              for (int k = NW / 4 * 4; k < NW; ++k) w[k] = lds_u32(rb + 4 * k);
+            } else {
+#pragma unroll
+              for (int k = 0; k < NW; ++k) w[k] = lds_u32(rb + 4 * k);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < NW; ++k) {
+              const int e = s_al + 2 * k;
+              // tensor-TMA stage: [box][row][BOXW]; 1D bulk stage: [row][ROW_ELEMS]
+              const int kb = p.use_tmap ? e / C::BOXW : 0;
+              const int bw = p.use_tmap ? C::BOXW : C::ROW_ELEMS;
+              w[k] = lds_u32(nbase + kb * p.box_slot + (b * bw + e - kb * bw) * 2);
+            }
           }
           const uint32_t gbase = sbase + (n / 8) * sbo + (n % 8) * 16 + b * KC * 128;
 #pragma unroll
@@ -1495,6 +1523,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
         return set_error(SPD_EUNSUPPORTED, "MMA start row mismatch (%d)", s);
   }
   sp.nat_bytes = sp.use_tmap ? sp.nbox * sp.box_slot : plan->g.r_in * C::ROW_BYTES;
+  if (sp.rowmajor) sp.nat_bytes = (sp.nbox * sp.boxw * 2 * plan->g.r_in + 127) / 128 * 128;
   if (!sp.use_tmap) {
     sp.nbox = 1;
     sp.boxw = C::ROW_ELEMS;
@@ -1616,6 +1645,21 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const int64_t rows = gd->plane / gd->pitch;
+  if (g.d == 2 && g.L != 4 && g.L != 8) {
+    // generic radii: one box per tile through the view (x, box, row) with
+    // box stride boxw elements, so the rows land contiguous in shared memory
+    cuuint64_t vdims[3] = {(cuuint64_t)gd->pitch, (cuuint64_t)sp.nbox, (cuuint64_t)rows};
+    cuuint64_t vstrides[2] = {(cuuint64_t)sp.boxw * 2, (cuuint64_t)gd->pitch * 2};
+    cuuint32_t vbox[3] = {(cuuint32_t)sp.boxw, (cuuint32_t)sp.nbox, (cuuint32_t)g.r_in};
+    cuuint32_t vestr[3] = {1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(buf), vdims, vstrides, vbox, vestr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled (row view) failed (%d)", (int)r);
+    sp.use_tmap = 1;
+    sp.rowmajor = 1;
+    return SPD_OK;
+  }
   cuuint64_t dims[3] = {(cuuint64_t)gd->pitch, (cuuint64_t)rows, (cuuint64_t)(gd->alloc_elems / gd->plane)};
   cuuint64_t strides[2] = {(cuuint64_t)gd->pitch * 2, (cuuint64_t)gd->plane * 2};
   cuuint32_t box[3] = {(cuuint32_t)sp.boxw, (cuuint32_t)(g.tile_y + 2 * g.r), (cuuint32_t)(g.tile_z + 2 * g.r)};
@@ -1932,7 +1976,9 @@ int spd_grid_layout(const spd_plan* plan, int64_t nz, int64_t ny, int64_t nx, in
   out->pitch = pitch;
   out->plane = rows * pitch;
   out->origin = zoff * out->plane + yoff * pitch + xoff;
-  out->alloc_elems = planes * out->plane;
+  // + slack: the generic-radius row view may read a few elements past the
+  // last padded row (boxes are rounded up to 8 elements)
+  out->alloc_elems = planes * out->plane + (plan->d == 2 ? 4096 : 0);
   return SPD_OK;
 }
 
