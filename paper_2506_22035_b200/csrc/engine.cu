@@ -821,6 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     bool valid[NQ];
     // natural stage: element x of row b at box k = x / boxw
     auto nat_addr = [&](int b, int x) -> uint32_t {
+      if (p.rowmajor) return (uint32_t)((b * p.nbox * p.boxw + x) * 2);  // contiguous rows
       const int k = x / p.boxw;
       return (uint32_t)(k * p.box_slot + (b * p.boxw + (x - k * p.boxw)) * 2);
     };
@@ -1645,7 +1646,8 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const int64_t rows = gd->plane / gd->pitch;
-  if (g.d == 2 && g.L != 4 && g.L != 8) {
+  static const char* rm_env = getenv("SPD_ROWMAJOR");  // development: row view for the fast paths too
+  if (g.d == 2 && ((g.L != 4 && g.L != 8) || (rm_env && atoi(rm_env) != 0))) {
     // generic radii: one box per tile through the view (x, box, row) with
     // box stride boxw elements, so the rows land contiguous in shared memory
     cuuint64_t vdims[3] = {(cuuint64_t)gd->pitch, (cuuint64_t)sp.nbox, (cuuint64_t)rows};
