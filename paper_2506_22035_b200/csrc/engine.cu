@@ -687,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           const int c0 = (int)(p.xoff + id.x0 - 8) + (int)crank * (NTILE * L);  // pair: x-half of this CTA
           const int c1 = (int)(p.yoff + id.y0 - g.r);
           const int c2 = (int)(p.zoff + id.z0 - g.r);
-          if (p.rowmajor) {
+          if (C::GEN && p.rowmajor) {
             tma_load_3d(dst, map, c0, 0, c1, fb);  // view (x, box, row): rows land contiguous
           } else {
             for (int k = 0; k < p.nbox; ++k) {
@@ -821,7 +821,6 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     bool valid[NQ];
     // natural stage: element x of row b at box k = x / boxw
     auto nat_addr = [&](int b, int x) -> uint32_t {
-      if (p.rowmajor) return (uint32_t)((b * p.nbox * p.boxw + x) * 2);  // contiguous rows
       const int k = x / p.boxw;
       return (uint32_t)(k * p.box_slot + (b * p.boxw + (x - k * p.boxw)) * 2);
     };
@@ -1646,8 +1645,7 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const int64_t rows = gd->plane / gd->pitch;
-  static const char* rm_env = getenv("SPD_ROWMAJOR");  // development: row view for the fast paths too
-  if (g.d == 2 && ((g.L != 4 && g.L != 8) || (rm_env && atoi(rm_env) != 0))) {
+  if (g.d == 2 && g.L != 4 && g.L != 8) {
     // generic radii: one box per tile through the view (x, box, row) with
     // box stride boxw elements, so the rows land contiguous in shared memory
     cuuint64_t vdims[3] = {(cuuint64_t)gd->pitch, (cuuint64_t)sp.nbox, (cuuint64_t)rows};
@@ -1980,7 +1978,7 @@ int spd_grid_layout(const spd_plan* plan, int64_t nz, int64_t ny, int64_t nx, in
   out->origin = zoff * out->plane + yoff * pitch + xoff;
   // + slack: the generic-radius row view may read a few elements past the
   // last padded row (boxes are rounded up to 8 elements)
-  out->alloc_elems = planes * out->plane + (plan->d == 2 ? 4096 : 0);
+  out->alloc_elems = planes * out->plane + (plan->d == 2 && plan->L != 4 && plan->L != 8 ? 4096 : 0);
   return SPD_OK;
 }
 
