@@ -1,0 +1,90 @@
+"""Full-size parity through the light cone (SURVEY.md §8(c) "Large grids").
+
+After T steps of a radius-r stencil, a point depends only on inputs within
+r*T of it.  So for the bench configurations at their full sizes and step
+counts (B9 / B49 at 10240^2, B27 at 512^3, T = 100):
+
+* the device result on the full grid, restricted to an inner block, equals
+  the device result on a crop holding that block plus an r*T margin
+  (the crop's outer ring acting as its Dirichlet halo) BIT FOR BIT — the
+  crop origin is tile-aligned, so every point sees the same arithmetic;
+* the crop is small enough for the C oracle (fp64 `naive_apply`, reference
+  core.py:151-182) to run the same T steps on the fp16-quantised inputs, so
+  the full-size result is pinned against the reference algorithm.  The
+  tolerance is the measured fp16 bound over 100 steps (max-rel, reference
+  pipeline.py:265-267): 2e-2, the same bound the 100-step Heat-3D test uses.
+
+Blocks are taken at the grid centre and at a corner (the global Dirichlet
+halo inside the light cone).
+"""
+import zlib
+
+import pytest
+import torch
+
+import bench
+import paper_2506_22035_b200 as sp
+from paper_2506_22035_b200.engine import DeviceGrid
+from paper_2506_22035_b200.pipeline import get_plan, max_rel_error
+from oracle import cnaive
+
+pytestmark = pytest.mark.gpu
+
+TOL_T100 = 2e-2
+
+
+@pytest.mark.parametrize("name,inner", [("B9", 64), ("B49", 32), ("B27", 16)])
+@pytest.mark.parametrize("where", ["centre", "corner"])
+@pytest.mark.timeout(600, method="thread")
+def test_light_cone_full_size(name, inner, where):
+    _, shape, d, r, kind, T = bench.CONFIGS[name]
+    kern = bench.make_kernel(kind, d, r)
+    plan = get_plan(kern, sp.Parity.EVEN, "fp16")
+    h, margin = r, r * T
+    gen = torch.Generator(device="cuda").manual_seed(zlib.crc32(f"{name}/{where}".encode()))
+    dense = torch.rand(tuple(n + 2 * h for n in shape), dtype=torch.float64, device="cuda",
+                       generator=gen) * 2 - 1
+    dense = dense.to(torch.float16).to(torch.float64)          # the inputs the device sees
+
+    full = DeviceGrid(plan, shape, h)
+    full.load_dense_f64(dense)
+    full.run(T)
+    out_full = full.to_dense_f64()
+    del full
+
+    # crop origin (dense index of its first halo point) tile-aligned with the
+    # full grid: 64 in x, 8 in y / z; the block sits `margin` points inside
+    if where == "centre":
+        cs = [(n // 2) // 8 * 8 for n in shape[:-1]] + [(shape[-1] // 2) // 64 * 64]
+    else:
+        cs = [0] * d                             # keeps the global halo as its own
+    lo = [c + margin for c in cs] if where == "centre" else [0] * d
+    size = [inner] * d
+    ext = [a + s + margin - c for c, a, s in zip(cs, lo, size)]     # crop interior extents
+    L = 2 * r + 2
+    ext[-1] = -(-ext[-1] // L) * L                                  # width: a multiple of L
+    sl = tuple(slice(c, min(c + e + 2 * h, n)) for c, e, n in zip(cs, ext, dense.shape))
+    crop_in = dense[sl].contiguous()
+    crop_shape = tuple(n - 2 * h for n in crop_in.shape)
+    offs = cs
+
+    cg = DeviceGrid(plan, crop_shape, h)
+    cg.load_dense_f64(crop_in)
+    cg.run(T)
+    out_crop = cg.to_dense_f64()
+    del cg
+
+    # the block inside the cone, in dense coordinates of each array
+    blk_full = tuple(slice(a + h, a + h + s) for a, s in zip(lo, size))
+    blk_crop = tuple(slice(a + h - o, a + h - o + s) for a, s, o in zip(lo, size, offs))
+    got_full = out_full[blk_full]
+    got_crop = out_crop[blk_crop]
+    assert torch.equal(got_full, got_crop), float((got_full - got_crop).abs().max())
+
+    # oracle on the crop (2D: all of it; 3D: the C oracle at 3D crop sizes is
+    # seconds too since the crop is (inner + 2rT)^3 = 216^3)
+    want = cnaive.naive_apply(kern.coeffs, d, r, crop_in.cpu().numpy(), h, T)
+    err = max_rel_error(got_crop.cpu().numpy(), want[blk_crop])
+    print(f"light-cone {name} {where}: max-rel vs fp64 oracle after T={T}: {err:.3e}")
+    assert err < TOL_T100, err
+    assert not torch.equal(got_crop, crop_in[blk_crop])            # the block did evolve
