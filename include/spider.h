@@ -18,7 +18,12 @@
  *   - spd_last_error() returns a thread-local message for the last failure.
  *   - Device pointers are owned by the caller (torch tensors); a plan owns only
  *     the packed A (compressed kernel) images and E (metadata) words.
- *   - One plan per device, stream-ordered, not thread-safe per plan.
+ *   - One plan per device, stream-ordered.  Per-step launches (spd_step,
+ *     spd_step_range, spd_run without SPD_RUN_PERSISTENT), copies and
+ *     naive_apply only read the plan, so several host threads may use one
+ *     plan at once on their own streams.  Persistent and ordered launches
+ *     (SPD_RUN_PERSISTENT, spd_step_ordered, spd_slab_step) use the plan's
+ *     completion counters: at most one of those in flight per plan.
  */
 #ifndef SPIDER_H
 #define SPIDER_H
@@ -194,6 +199,15 @@ int spd_upload(const spd_grid_desc* g, const void* host_dense, void* dev,
                void* stream);
 int spd_download(const spd_grid_desc* g, const void* dev, void* host_dense,
                  void* stream);
+
+/* Same transfers through a caller-owned device staging buffer of the dense
+ * size ((nz+2h)(ny+2h)(nx+2h) 16-bit elements): one linear DMA plus a
+ * device repack kernel, stream-ordered.  Faster than the strided DMA when
+ * rows are short (3D grids: ~1 KB rows). */
+int spd_upload_staged(const spd_grid_desc* g, const void* host_dense,
+                      void* dev, void* staging, void* stream);
+int spd_download_staged(const spd_grid_desc* g, const void* dev,
+                        void* host_dense, void* staging, void* stream);
 
 /* Device fp64 brute-force executor: naive_apply (core.py:151-182) on the
  * natural dense layout, same row-major tap order, separate multiply and add

@@ -81,6 +81,8 @@ SIGNATURES = {
     "spd_unpack_grid": (_I, [_DESC, _I, _P, _P, _P]),
     "spd_upload": (_I, [_DESC, _P, _P, _P]),
     "spd_download": (_I, [_DESC, _P, _P, _P]),
+    "spd_upload_staged": (_I, [_DESC, _P, _P, _P, _P]),
+    "spd_download_staged": (_I, [_DESC, _P, _P, _P, _P]),
     "spd_naive_apply_f64": (_I, [_I, _I, _D, _I64, _I64, _I64, _I, _P, _P, _P, _I, _P]),
     "spd_mma_selftest": (_I, [_P, _P, _P, _I, _P, _P]),
     "spd_halo_pack": (_I, [_DESC, _P, _I, _I, _P, _P]),

@@ -2147,6 +2147,54 @@ int spd_download(const spd_grid_desc* g, const void* dev, void* host_dense, void
   return spd::cuda_err(cudaMemcpy3DAsync(&p, (cudaStream_t)stream), "spd_download");
 }
 
+// Staged transfers: one linear DMA between the host dense array and a
+// device staging buffer of the same (dense) layout at full PCIe rate, plus a
+// row-wise repack kernel on the device.  A strided cudaMemcpy3D moves one
+// (nx+2h)-element row per DMA descriptor, which for the 3D grids' ~1 KB rows
+// runs at a fraction of the link rate.
+namespace spd {
+__global__ void repack_rows_kernel(DenseMap dm, int64_t pitch, int64_t plane, int64_t origin, const uint16_t* src,
+                                   uint16_t* dst, bool to_dev) {
+  const int64_t rows = dm.nzd * dm.nyd;
+  const int64_t z0 = dm.d == 3 ? dm.h : 0;
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t zz = row / dm.nyd, yy = row - zz * dm.nyd;
+    const int64_t dense0 = row * dm.nxd;
+    const int64_t dev0 = origin + (zz - z0) * plane + (yy - dm.h) * pitch - dm.h;
+    if (to_dev)
+      for (int64_t x = threadIdx.x; x < dm.nxd; x += blockDim.x) dst[dev0 + x] = src[dense0 + x];
+    else
+      for (int64_t x = threadIdx.x; x < dm.nxd; x += blockDim.x) dst[dense0 + x] = src[dev0 + x];
+  }
+}
+}  // namespace spd
+
+static int64_t dense_elems(const spd_grid_desc* g) {
+  const int64_t h = g->halo;
+  return (g->dims == 3 ? g->nz + 2 * h : 1) * (g->ny + 2 * h) * (g->nx + 2 * h);
+}
+
+int spd_upload_staged(const spd_grid_desc* g, const void* host_dense, void* dev, void* staging, void* stream) {
+  if (!g || !host_dense || !dev || !staging) return spd::set_error(SPD_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemcpyAsync(staging, host_dense, (size_t)dense_elems(g) * 2, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return spd::cuda_err(e, "spd_upload_staged copy");
+  spd::repack_rows_kernel<<<148 * 8, 256, 0, st>>>(dense_map(g, g->dims), g->pitch, g->plane, g->origin,
+                                                   (const uint16_t*)staging, (uint16_t*)dev, true);
+  return spd::cuda_err(cudaGetLastError(), "repack_rows_kernel");
+}
+
+int spd_download_staged(const spd_grid_desc* g, const void* dev, void* host_dense, void* staging, void* stream) {
+  if (!g || !host_dense || !dev || !staging) return spd::set_error(SPD_EINVAL, "null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  spd::repack_rows_kernel<<<148 * 8, 256, 0, st>>>(dense_map(g, g->dims), g->pitch, g->plane, g->origin,
+                                                   (const uint16_t*)dev, (uint16_t*)staging, false);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(host_dense, staging, (size_t)dense_elems(g) * 2, cudaMemcpyDeviceToHost, st);
+  return spd::cuda_err(e, "spd_download_staged");
+}
+
 int spd_naive_apply_f64(int d, int r, const double* coeffs, int64_t nz, int64_t ny, int64_t nx, int halo,
                         const double* in, double* out, double* scratch, int steps, void* stream) {
   using namespace spd;

@@ -9,6 +9,7 @@ path here falls back to the host.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -165,21 +166,50 @@ class DeviceGrid:
                                   _stream_ptr(stream)))
         return out
 
-    def upload(self, host: torch.Tensor, stream=None) -> None:
-        """Strided DMA of a host 16-bit dense grid (pinned for async)."""
+    def _staged(self, staged) -> bool:
+        """Host transfers through a device staging buffer (one linear DMA +
+        a repack kernel) instead of a strided DMA: the default for short rows
+        (3D grids), where the strided copy engine path is slow."""
+        if staged is None:
+            env = os.environ.get("SPD_STAGED")
+            staged = bool(int(env)) if env else (self.desc.dims == 3 or self.dense_shape[-1] * 2 < 16384)
+        return staged
+
+    def _staging(self, stream):
+        buf = torch.empty(self.dense_shape, dtype=TORCH_DTYPES[self.plan.dtype], device=self.bufs[0].device)
+        if stream is not None:
+            buf.record_stream(stream)
+        return buf
+
+    def upload(self, host: torch.Tensor, stream=None, staged=None) -> None:
+        """DMA of a host 16-bit dense grid (pinned for async)."""
         if host.dtype != TORCH_DTYPES[self.plan.dtype] or host.is_cuda:
             raise ValueError(f"expected a host {TORCH_DTYPES[self.plan.dtype]} tensor")
         if tuple(host.shape) != tuple(self.dense_shape) or not host.is_contiguous():
             raise ValueError(f"host grid must be contiguous with shape {self.dense_shape}")
-        check(lib.spd_upload(C.byref(self.desc), C.c_void_p(host.data_ptr()),
-                             C.c_void_p(self.bufs[self.cur].data_ptr()), _stream_ptr(stream)))
+        if self._staged(staged):
+            st = self._staging(stream)
+            check(lib.spd_upload_staged(C.byref(self.desc), C.c_void_p(host.data_ptr()),
+                                        C.c_void_p(self.bufs[self.cur].data_ptr()), C.c_void_p(st.data_ptr()),
+                                        _stream_ptr(stream)))
+        else:
+            check(lib.spd_upload(C.byref(self.desc), C.c_void_p(host.data_ptr()),
+                                 C.c_void_p(self.bufs[self.cur].data_ptr()), _stream_ptr(stream)))
         self._sync_halo(stream)
 
-    def download(self, host: torch.Tensor, stream=None) -> None:
+    def download(self, host: torch.Tensor, stream=None, staged=None) -> None:
         if host.dtype != TORCH_DTYPES[self.plan.dtype] or host.is_cuda:
             raise ValueError(f"expected a host {TORCH_DTYPES[self.plan.dtype]} tensor")
-        check(lib.spd_download(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
-                               C.c_void_p(host.data_ptr()), _stream_ptr(stream)))
+        if tuple(host.shape) != tuple(self.dense_shape) or not host.is_contiguous():
+            raise ValueError(f"host grid must be contiguous with shape {self.dense_shape}")
+        if self._staged(staged):
+            st = self._staging(stream)
+            check(lib.spd_download_staged(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
+                                          C.c_void_p(host.data_ptr()), C.c_void_p(st.data_ptr()),
+                                          _stream_ptr(stream)))
+        else:
+            check(lib.spd_download(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
+                                   C.c_void_p(host.data_ptr()), _stream_ptr(stream)))
 
     def run(self, steps: int, stream=None, persistent: bool = False) -> None:
         """`steps` Jacobi steps on the device, ping-ponging the buffers

@@ -19,6 +19,7 @@ hot path moved to the B200:
 from __future__ import annotations
 
 import json
+import threading
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -157,15 +158,20 @@ def transform_stencil(kernel: StencilKernel, cfg=ExecConfig()) -> TransformedSte
 # plan cache (one per kernel/parity/dtype/device)
 
 _PLANS: dict = {}
+_PLANS_LOCK = threading.Lock()
 
 
 def get_plan(kernel: StencilKernel, parity: Parity, dtype: str, device: int | None = None) -> Plan:
+    """Cached plan.  Plans are read-only once built, so `execute` may be
+    called from several host threads at once (each on its own current CUDA
+    stream), as the reference's pure functions may."""
     dev = require_cuda(device).index if device is None else int(device)
     key = (kernel.d, kernel.r, np.asarray(kernel.coeffs, dtype=np.float64).tobytes(), Parity(parity), dtype, dev)
-    plan = _PLANS.get(key)
-    if plan is None:
-        plan = Plan(kernel, parity, dtype, dev)
-        _PLANS[key] = plan
+    with _PLANS_LOCK:
+        plan = _PLANS.get(key)
+        if plan is None:
+            plan = Plan(kernel, parity, dtype, dev)
+            _PLANS[key] = plan
     return plan
 
 

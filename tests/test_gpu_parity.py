@@ -243,18 +243,25 @@ def test_step_range_composes_to_full_step():
     assert torch.equal(a.bufs[a.cur], b.bufs[b.cur])
 
 
-def test_upload_download_roundtrip():
-    k = rand_kernel("box", 2, 3, seed=3)
+@pytest.mark.parametrize("d,r,shape", [(2, 3, (100, 264)), (2, 1, (37, 4096)), (3, 1, (9, 20, 72)), (1, 2, (1, 600))])
+@pytest.mark.parametrize("staged", [False, True])
+def test_upload_download_roundtrip(d, r, shape, staged):
+    """Strided DMA and staged (linear DMA + repack kernel) transfers place
+    every element, halo included, identically; the two are interchangeable."""
+    k = rand_kernel("box", d, r, seed=3)
     plan = get_plan(k, sp.Parity.EVEN, "fp16")
-    dg = DeviceGrid(plan, (100, 264), 3)
+    dg = DeviceGrid(plan, shape, r)
     host = torch.randn(dg.dense_shape, dtype=torch.float16).pin_memory()
-    dg.upload(host)
-    back = torch.empty_like(host)
-    dg.download(back)
+    dg.upload(host, staged=staged)
+    back = torch.empty_like(host).pin_memory()
+    dg.download(back, staged=not staged)
     torch.cuda.synchronize()
     assert torch.equal(host, back)
     dense = dg.to_dense_f64().cpu()
     assert torch.equal(dense, host.to(torch.float64))
+    dg.download(back.zero_(), staged=staged)
+    torch.cuda.synchronize()
+    assert torch.equal(host, back)
 
 
 def test_reference_error_contract():
