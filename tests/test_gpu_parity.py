@@ -505,3 +505,32 @@ def test_cta_pair_3d_bit_identical(monkeypatch, shape):
         g.run(3)
         outs.append(g.to_dense_f64())
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("d,r,dims", [(2, 1, (96, 1024)), (3, 1, (24, 24, 256))])
+def test_concurrent_execute_callers(d, r, dims):
+    """execute() from several host threads at once (each on its own stream,
+    sharing one cached plan) gives the same bits as sequential calls."""
+    import threading
+
+    k = rand_kernel("box", d, r, seed=[d, 11])
+    cls = sp.Grid3D if d == 3 else sp.Grid
+    grids = []
+    for i in range(4):
+        data = quant(np.random.default_rng(i).uniform(-1, 1, tuple(n + 2 * r for n in dims))).astype(np.float16)
+        grids.append(cls(data, r))
+    want = [sp.execute(k, g, 5)[0].data.copy() for g in grids]
+    got = [None] * len(grids)
+
+    def worker(i):
+        with torch.cuda.stream(torch.cuda.Stream()):
+            for _ in range(3):
+                got[i] = sp.execute(k, grids[i], 5)[0].data.copy()
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(grids))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    for w, g in zip(want, got):
+        np.testing.assert_array_equal(g, w)
