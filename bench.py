@@ -459,7 +459,10 @@ def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
         threads = [threading.Thread(target=worker, args=(i,)) for i in range(n_callers)]
         for t in threads:
             t.start()
-        start.wait()
+        try:
+            start.wait()
+        except threading.BrokenBarrierError:
+            pass  # a worker failed; its exception is re-raised below
         t0 = time.perf_counter()
         for t in threads:
             t.join()
