@@ -1,13 +1,19 @@
-"""Benchmark of the SPIDER hot path on B200 (contract: see DESIGN.md §Measurement).
+"""Benchmark of the SPIDER hot path on B200 (contract: DESIGN.md §6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config B9|B49|B27|B25|W|S5]
-                    [--impl ours|reference] [--no-cpu-baseline]
+                    [--impl ours|reference] [--no-cpu-baseline] [--no-e2e] [--no-configs]
 
 One bench "step" = one pass of the configuration over its grid: T Jacobi
 timesteps of the stencil (T = 100 for B9/B27/B49/W).  Per GPU the grid is the
 configuration's grid (weak scaling: N ranks own N slabs of that size, stacked
-along y / z, with one NCCL halo exchange per timestep).  Metric: GStencil/s =
+along y / z, with one halo exchange per timestep).  Metric: GStencil/s =
 points x timesteps / device time, whole job (all ranks), max over ranks.
+
+`--gpus N` with no launcher environment (WORLD_SIZE unset) starts the N ranks
+itself (one process per GPU, 127.0.0.1 rendezvous); under torchrun it uses the
+launcher's ranks.  The default line (B9) carries a `configs` block with the
+other BASELINE configurations (B49, B27, W; at N > 1 the W weak-scaling
+configuration) measured in the same run.
 
 `--impl reference` times the reference algorithm's CPU implementation (the
 oracle's C port of naive_apply, all host threads) on the same config.
@@ -17,6 +23,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,6 +46,8 @@ CONFIGS = {
     "B25": ("Box-2D25P (5x5) fp16 10240x10242, 100 timesteps", (10240, 10242), 2, 2, "box", 100),
     "W": ("Box-2D9P fp16 16384x16384 per GPU, 100 timesteps", (16384, 16384), 2, 1, "box", 100),
 }
+# measured alongside the headline configuration in the default run
+SIDE_CONFIGS = {1: ("B49", "B27", "W"), "multi": ("W",)}
 
 
 def coefficients(kind: str, d: int, r: int, seed: int = 1):
@@ -62,8 +71,17 @@ def make_kernel(kind, d, r):
     return sp.make_kernel_3d(shape, r, c) if d == 3 else sp.make_kernel(shape, d, r, c)
 
 
+def workload_config(cfg_name: str, world: int) -> dict:
+    """The workload description both arms print (`config`)."""
+    desc, shape, d, r, kind, T = CONFIGS[cfg_name]
+    dense = tuple(s + 2 * r for s in shape)
+    return {"workload": cfg_name, "description": desc, "grid_per_gpu": list(shape), "timesteps_per_step": T,
+            "parallelism": f"slab{world}" if world > 1 else "single",
+            "l2": f"inputs larger than L2 ({2 * np.prod(dense) / 2**20:.0f} MiB per fp16 buffer)"}
+
+
 # ---------------------------------------------------------------------------
-# clocks sampling (nvidia-smi during the timed region)
+# clocks sampling (NVML during the timed region)
 
 class ClockSampler:
     """Samples SM clock and throttle reasons through NVML (every 10 ms) while
@@ -141,37 +159,13 @@ def ncu_traffic(config: str):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (reference algorithm, oracle C port, all host threads)
+# CPU reference algorithm (oracle C port of naive_apply, all host threads)
 
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
     except AttributeError:
         return os.cpu_count() or 1
-
-
-def cpu_reference_rate(cfg_name: str, budget_s: float = 10.0):
-    """GStencil/s of the oracle C port on a bounded sample of the workload:
-    the full grid, as many timesteps as fit in ~budget_s (>= 1)."""
-    from oracle import cnaive
-
-    desc, shape, d, r, kind, T = CONFIGS[cfg_name]
-    coeffs = coefficients(kind, d, r)
-    rng = np.random.default_rng(0)
-    dense = rng.uniform(-1, 1, tuple(s + 2 * r for s in shape))
-    threads = cpu_threads()
-    points = int(np.prod(shape))
-    t0 = time.perf_counter()
-    cnaive.naive_apply(coeffs, d, r, dense, r, 1, threads=threads)
-    t1 = time.perf_counter() - t0
-    steps = max(1, min(T, int(budget_s / max(t1, 1e-6))))
-    if steps > 1:
-        t0 = time.perf_counter()
-        cnaive.naive_apply(coeffs, d, r, dense, r, steps, threads=threads)
-        t1 = time.perf_counter() - t0
-    else:
-        steps = 1
-    return points * steps / t1 / 1e9, threads, f"{shape} grid x {steps} timestep(s), {t1:.2f} s wall, fp64"
 
 
 def cpu_model():
@@ -184,32 +178,56 @@ def cpu_model():
     return "unknown"
 
 
-# ---------------------------------------------------------------------------
+def cpu_runner(cfg_name: str):
+    """Resident two-buffer fp64 grid of the workload for the C port."""
+    from oracle import cnaive
+
+    desc, shape, d, r, kind, T = CONFIGS[cfg_name]
+    rng = np.random.default_rng(0)
+    dense = rng.uniform(-1, 1, tuple(s + 2 * r for s in shape))
+    threads = cpu_threads()
+    return cnaive.NaiveRunner(coefficients(kind, d, r), d, r, dense, r, threads=threads), threads
+
+
+def cpu_reference_rate(cfg_name: str, budget_s: float = 10.0):
+    """GStencil/s of the oracle C port on a bounded sample of the workload:
+    the full grid, as many timesteps as fit in ~budget_s (>= 1), buffers
+    allocated and warmed before timing."""
+    desc, shape, d, r, kind, T = CONFIGS[cfg_name]
+    runner, threads = cpu_runner(cfg_name)
+    points = int(np.prod(shape))
+    t0 = time.perf_counter()
+    runner.run(1)  # warm: page-faults both buffers, spins up the threads
+    t1 = time.perf_counter() - t0
+    steps = max(1, min(T, int(budget_s / max(t1, 1e-6))))
+    t0 = time.perf_counter()
+    runner.run(steps)
+    el = time.perf_counter() - t0
+    return points * steps / el / 1e9, threads, f"{shape} grid x {steps} timestep(s), {el:.2f} s wall, fp64"
+
 
 def run_reference(args, cfg_name):
+    """Reference arm: one bench step = the workload's T timesteps over the
+    full grid (same work per step as our arm), on two resident fp64 buffers.
+    Warm-up steps run one timestep each (buffer page-in, thread spin-up)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     desc, shape, d, r, kind, T = CONFIGS[cfg_name]
-    from oracle import cnaive
-
-    coeffs = coefficients(kind, d, r)
-    rng = np.random.default_rng(0)
-    dense = rng.uniform(-1, 1, tuple(s + 2 * r for s in shape))
-    threads = cpu_threads()
+    runner, threads = cpu_runner(cfg_name)
     points = int(np.prod(shape))
-    # one bench step = `ts` timesteps over the full grid in one call (a
-    # bounded sample of the T-timestep workload, ~5e8 point updates, so the
-    # per-call grid copies of the C port are amortised like the workload's)
-    ts = max(1, min(T, int(round(5e8 / points))))
     for _ in range(args.warmup):
-        cnaive.naive_apply(coeffs, d, r, dense, r, ts, threads=threads)
+        runner.run(1)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cnaive.naive_apply(coeffs, d, r, dense, r, ts, threads=threads)
+        runner.run(T)
     el = time.perf_counter() - t0
-    value = points * ts * args.steps / el / 1e9
-    sample = f"{shape} grid x {ts} timestep(s) per step ({args.steps} steps), fp64, {cpu_model()}"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    # whole-job work of the configuration at N GPUs (weak scaling: N grids),
+    # done by the host cores on rank 0
+    value = points * T * args.steps / el / 1e9
+    sample = (f"{shape} grid x {T} timesteps per step ({args.steps} steps, resident buffers), fp64, "
+              f"{cpu_model()}")
     line = {
         "impl": "reference",
         "metric": f"GStencil/s ({desc})",
@@ -224,7 +242,7 @@ def run_reference(args, cfg_name):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic U(-1,1) grid, contractive normalised weights",
-        "config": {"workload": cfg_name, "description": desc, "grid": list(shape), "timesteps": T},
+        "config": workload_config(cfg_name, world),
         "cpu_baseline": {"value": round(value, 5), "unit": "GStencil/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(value, 5), "unit": "GStencil/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -233,47 +251,70 @@ def run_reference(args, cfg_name):
     return 0
 
 
-def run_ours(args, cfg_name):
+# ---------------------------------------------------------------------------
+# our arm
+
+class Ctx:
+    """Per-process distributed context."""
+
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", "0"))
+        if self.world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={self.world}")
+        # SPD_BENCH_BACKEND=gloo lets several ranks share one GPU (functional
+        # checks of the multi-rank path on a 1-GPU box; timings then mean nothing)
+        self.backend = os.environ.get("SPD_BENCH_BACKEND", "nccl")
+        self.local = local % torch.cuda.device_count()
+        torch.cuda.set_device(self.local)
+        if self.world > 1:
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                dist.init_process_group(self.backend)
+        self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[self.local])
+            else:
+                self.dist.barrier()
+
+    def max_over_ranks(self, v: float) -> float:
+        import torch
+
+        if self.world == 1:
+            return v
+        t = torch.tensor([v], device="cuda" if self.backend == "nccl" else "cpu", dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+def measure(ctx: Ctx, args, cfg_name: str, exchange: str) -> dict:
+    """Device-timed throughput of one configuration (all ranks)."""
     import torch
-    import torch.distributed as dist
 
     import paper_2506_22035_b200 as sp
     from paper_2506_22035_b200.engine import DeviceGrid
     from paper_2506_22035_b200.pipeline import get_plan
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    # SPD_BENCH_BACKEND=gloo lets several ranks share one GPU (functional
-    # checks of the multi-rank path on a 1-GPU box; timings then mean nothing)
-    backend = os.environ.get("SPD_BENCH_BACKEND", "nccl")
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+    world, rank = ctx.world, ctx.rank
     desc, shape, d, r, kind, T = CONFIGS[cfg_name]
     kern = make_kernel(kind, d, r)
-    plan = get_plan(kern, sp.Parity.EVEN, "fp16", local)
+    plan = get_plan(kern, sp.Parity.EVEN, "fp16", ctx.local)
     info = plan.info()
     points_local = int(np.prod(shape))
     stream = torch.cuda.current_stream()
-
-    def barrier():
-        if world > 1:
-            if backend == "nccl":
-                dist.barrier(device_ids=[local])
-            else:
-                dist.barrier()
-
     gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
     dense_shape = tuple(s + 2 * r for s in shape)
     peer = None
-    if world == 1 and not args.force_slab:
+    slab_mode = world > 1 or args.force_slab
+    if not slab_mode:
         grid = DeviceGrid(plan, shape, r)
         dense = torch.rand(dense_shape, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
         grid.load_dense_f64(dense)
@@ -281,7 +322,6 @@ def run_ours(args, cfg_name):
         launches_per_step = T
         if args.graph:
             graph = torch.cuda.CUDAGraph()
-            # capture T steps (an even T keeps the buffer parity fixed per replay)
             s = torch.cuda.Stream()
             s.wait_stream(stream)
             with torch.cuda.stream(s):
@@ -295,12 +335,11 @@ def run_ours(args, cfg_name):
                 graph.replay()
         else:
             # T step kernels straight into the stream: consecutive launches
-            # overlap through programmatic dependent launch (measured faster
-            # than a CUDA-graph replay of the same T launches)
+            # overlap through programmatic dependent launch
             def one_step():
                 grid.run(T)
     else:
-        from paper_2506_22035_b200.distributed import DeviceSlabOps, Slab, SlabDriver
+        from paper_2506_22035_b200.distributed import DeviceSlabOps, PeerSlab, Slab, SlabDriver
 
         ops = DeviceSlabOps(plan, shape, r)
         dense = torch.rand(dense_shape, dtype=torch.float64, device="cuda", generator=gen) * 2 - 1
@@ -312,16 +351,15 @@ def run_ours(args, cfg_name):
         drv = SlabDriver(slab, ops, comm_stream=comm, compute_stream=stream)
         boundary, interior = drv._bands()
         launches_per_step = T * (len(boundary) + len(interior))
-        if args.exchange == "peer":
+        if exchange == "peer":
             # halos through peer memory (CUDA IPC + stream memory operations):
-            # one host call per timestep, no NCCL on the data path
-            from paper_2506_22035_b200.distributed import PeerSlab
-
+            # one host call and one launch per timestep, no NCCL on the data path
             try:
                 peer = PeerSlab(plan, slab, ops.grid, compute_stream=stream, comm_stream=comm)
-            except Exception as exc:  # IPC unavailable: NCCL send/recv driver
+                launches_per_step = T
+            except Exception as exc:  # IPC / peer access unavailable: NCCL send/recv driver (all ranks)
                 print(f"peer exchange unavailable ({exc}); using NCCL send/recv", file=sys.stderr)
-                args.exchange = "nccl"
+                exchange = "nccl"
 
         def one_step():
             if peer is not None:
@@ -334,52 +372,72 @@ def run_ours(args, cfg_name):
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
-    barrier()
+    ctx.barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(ctx.local) as clk:
         torch.cuda.synchronize()
-        barrier()
+        ctx.barrier()
         e0.record(stream)
         for _ in range(args.steps):
             one_step()
         e1.record(stream)
         torch.cuda.synchronize()
-        barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda" if backend == "nccl" else "cpu", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / args.steps
+        ctx.barrier()
+    ms = ctx.max_over_ranks(e0.elapsed_time(e1))
     value = world * points_local * T * args.steps / (ms / 1e3) / 1e9
 
     # roofline of the dominant kernel (the step kernel): algorithmic 4 B per
-    # point per timestep (fp16 read + write), SURVEY.md §8(d)
+    # point per timestep (fp16 read + write); in one-grid mode
+    # the timed region is nothing but the T x K step launches on this stream
     hbm, peak_kind = measured_peaks()
     n_launch = args.steps * T
-    slab_mode = world > 1 or args.force_slab
-    launch_s = (ms / 1e3) / n_launch if not slab_mode else None
-    if not slab_mode:
-        achieved = 4.0 * points_local / launch_s / 1e9
-    else:
-        achieved = 4.0 * points_local * T * args.steps / (ms / 1e3) / 1e9
+    launch_s = (ms / 1e3) / n_launch
+    achieved = 4.0 * points_local / launch_s / 1e9
     traffic, traffic_src = ncu_traffic(cfg_name)
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                 "frac": round(achieved / hbm, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": 4 * points_local,
-                "avg_launch_us": round(launch_s * 1e6, 2) if launch_s else None,
+                "avg_launch_us": round(launch_s * 1e6, 2),
+                "timing": ("step kernel launches only" if not slab_mode else
+                           "slab steps (step kernel + halo exchange) per timestep"),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})", "traffic_source": traffic_src}
+    if peer is not None:
+        ctx.barrier()
+        peer.close()
+    res = {"value": round(value, 2), "ms_per_step": round(ms / args.steps, 4), "roofline": roofline,
+           "clocks": clk.summary(), "gpu_launches": args.steps * launches_per_step,
+           "impl_detail": {"launch": "cuda-graph" if args.graph else "stream, programmatic dependent launch",
+                           "exchange": exchange if slab_mode else None,
+                           "tile": {"L": info.L, "n_tile": info.n_tile, "mmas_per_tile": info.mmas_per_tile,
+                                    "m_tiles": info.m_tiles}}}
+    del plan
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args, cfg_name):
+    import torch
+
+    import paper_2506_22035_b200 as sp
+
+    ctx = Ctx(args)
+    world, rank = ctx.world, ctx.rank
+    desc, shape, d, r, kind, T = CONFIGS[cfg_name]
+    head = measure(ctx, args, cfg_name, args.exchange)
+
+    side = {}
+    if not args.no_configs and cfg_name == "B9":
+        for name in SIDE_CONFIGS[1 if world == 1 else "multi"]:
+            side[name] = measure(ctx, args, name, args.exchange)
+            side[name]["config"] = workload_config(name, world)
 
     # end to end through the public API: pinned host fp16 grid in, result out.
-    # Every call is a full execute() (H2D of its grid, T steps, D2H of the
-    # result); `callers` host threads issue calls concurrently, each on its own
-    # CUDA stream with its own pinned buffers, so one call's copies overlap
-    # another's steps (PCIe is full duplex) -- the way a server drives the
-    # engine.  Wall-clock over all calls; the one-caller figure is kept too.
     e2e = None
     if rank == 0 and world == 1 and not args.no_e2e and not args.force_slab:
-        e2e = e2e_rate(sp, kern, d, r, dense_shape, T, points_local, args.e2e_callers,
+        points_local = int(np.prod(shape))
+        dense_shape = tuple(s + 2 * r for s in shape)
+        e2e = e2e_rate(sp, make_kernel(kind, d, r), d, r, dense_shape, T, points_local, args.e2e_callers,
                        max(2, min(args.steps, 4)))
 
     cpu = None
@@ -389,45 +447,42 @@ def run_ours(args, cfg_name):
                "sample": sample + f", {cpu_model()}"}
 
     if rank == 0:
-        slab = "x".join(str(s) for s in shape)
         line = {
             "metric": f"GStencil/s ({desc})",
-            "value": round(value, 2),
+            "value": head["value"],
             "unit": "GStencil/s",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
-            "ms_per_step": round(ms_per_step, 4),
+            "ms_per_step": head["ms_per_step"],
             "higher_is_better": True,
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "fp16",
             "data": "synthetic U(-1,1) grid, contractive normalised weights (random init)",
-            "config": {"workload": cfg_name, "description": desc, "grid_per_gpu": list(shape),
-                       "timesteps_per_step": T, "parallelism": f"slab{world}" if slab_mode else "single",
-                       "launch": "cuda-graph" if args.graph else "stream, programmatic dependent launch",
-                       "exchange": (args.exchange if slab_mode else None),
-                       "l2": f"inputs larger than L2 ({2 * np.prod(dense_shape) / 2**20:.0f} MiB per buffer)",
-                       "tile": {"L": info.L, "n_tile": info.n_tile, "mmas_per_tile": info.mmas_per_tile},
-                       "slab": slab},
-            "roofline": roofline,
+            "config": workload_config(cfg_name, world),
+            "impl_detail": head["impl_detail"],
+            "roofline": head["roofline"],
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": n_launch if not slab_mode else args.steps * launches_per_step,
-            "clocks": clk.summary(),
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
         }
+        if side:
+            line["configs"] = side
         print(json.dumps(line), flush=True)
-    if peer is not None:
-        barrier()
-        peer.close()
     if world > 1:
-        dist.destroy_process_group()
+        ctx.dist.destroy_process_group()
     return 0
 
 
 def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
-    """End-to-end GStencil/s through `sp.execute` with host buffers (see main)."""
-    import numpy as np
+    """End-to-end GStencil/s through `sp.execute` with host buffers.  Every
+    call is a full execute() (H2D of its grid, T steps, D2H of the result);
+    `callers` host threads issue calls concurrently, each on its own CUDA
+    stream with its own pinned buffers, so one call's copies overlap another's
+    steps (PCIe is full duplex) -- the way a server drives the engine.  Wall
+    clock over all calls; the one-caller figure is kept too."""
     import torch
 
     cls = sp.Grid3D if d == 3 else sp.Grid
@@ -448,7 +503,7 @@ def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
             try:
                 with torch.cuda.stream(streams[i]):
                     g_in, g_out = bufs[i]
-                    sp.execute(kern, g_in, T, out=g_out)  # warm (allocator, stream)
+                    sp.execute(kern, g_in, T, out=g_out)  # warm (allocator, stream, grid cache)
                     start.wait()
                     for _ in range(n_calls):
                         sp.execute(kern, g_in, T, out=g_out)
@@ -482,6 +537,29 @@ def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
             "api": "paper_2506_22035_b200.execute(kernel, Grid(pinned fp16), T, out=Grid(pinned fp16))"}
 
 
+# ---------------------------------------------------------------------------
+# self-launch of N ranks (no torchrun in the environment)
+
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """Re-run this command as n rank processes (RANK/LOCAL_RANK/WORLD_SIZE,
+    127.0.0.1 rendezvous); rank 0's stdout carries the JSON line."""
+    port = str(_free_port())
+    procs = []
+    for rank in range(n):
+        env = dict(os.environ, RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=port)
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *sys.argv[1:]], env=env))
+    rcs = [p.wait() for p in procs]
+    bad = [rc for rc in rcs if rc != 0]
+    return bad[0] if bad else 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -491,6 +569,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the side configurations block")
     ap.add_argument("--e2e-callers", type=int, default=3,
                     help="host threads issuing concurrent execute() calls in the e2e measurement")
     ap.add_argument("--force-slab", action="store_true", help="use the multi-GPU slab driver even at N=1")
@@ -500,6 +579,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args, args.config)
     return run_ours(args, args.config)

@@ -109,6 +109,13 @@ typedef struct spd_plan spd_plan;
 
 int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype,
                     int device, spd_plan** out);
+/* spd_plan_create with geometry flags.  SPD_PLAN_CTA_PAIR (3D only): one
+ * M = 256 tcgen05.mma.sp.cta_group::2 per K-block on a cluster of two CTAs
+ * (measured slower than the default two-M-tile CTA; kept for experiments).
+ * The geometry depends only on (d, r, flags), never on the environment. */
+#define SPD_PLAN_CTA_PAIR 1
+int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype,
+                       int device, int flags, spd_plan** out);
 int spd_plan_destroy(spd_plan* plan);
 
 /* Introspection of the packed operands (for the exact-layout tests).
@@ -208,6 +215,12 @@ int spd_upload_staged(const spd_grid_desc* g, const void* host_dense,
                       void* dev, void* staging, void* stream);
 int spd_download_staged(const spd_grid_desc* g, const void* dev,
                         void* host_dense, void* staging, void* stream);
+
+/* Copy the Dirichlet ring (halo rows, planes and columns of the dense
+ * region; not the interior) of a grid from one device buffer to another of
+ * the same layout: after a host upload into one ping-pong buffer, the other
+ * needs the same halo before the second step reads it.  16-bit elements. */
+int spd_copy_halo(const spd_grid_desc* g, const void* src, void* dst, void* stream);
 
 /* Device fp64 brute-force executor: naive_apply (core.py:151-182) on the
  * natural dense layout, same row-major tap order, separate multiply and add

@@ -44,6 +44,60 @@ static void* worker(void* arg) {
   return NULL;
 }
 
+static void tap_offsets(int d, int r, int64_t nyd, int64_t nxd, int64_t* off) {
+  int t = 0;
+  if (d == 1) {
+    for (int dx = -r; dx <= r; ++dx) off[t++] = dx;
+  } else if (d == 2) {
+    for (int ry = -r; ry <= r; ++ry)
+      for (int dx = -r; dx <= r; ++dx) off[t++] = (int64_t)ry * nxd + dx;
+  } else {
+    for (int rz = -r; rz <= r; ++rz)
+      for (int ry = -r; ry <= r; ++ry)
+        for (int dx = -r; dx <= r; ++dx) off[t++] = ((int64_t)rz * nyd + ry) * nxd + dx;
+  }
+}
+
+/* Jacobi steps on two caller-owned dense buffers (both holding the halo):
+ * step s reads bufs[s % 2] and writes bufs[(s + 1) % 2]; no copies, no
+ * allocation of grid-sized memory (the bench's CPU-baseline arm).  Returns the
+ * index (0 = a, 1 = b) of the buffer holding the result, or -1. */
+int oracle_naive_steps(int d, int r, const double* coeffs, int64_t nz, int64_t ny, int64_t nx, int halo, double* a,
+                       double* b, int steps, int threads) {
+  if (steps < 1 || halo < r || d < 1 || d > 3) return -1;
+  if (threads < 1) threads = 1;
+  int span = 2 * r + 1;
+  int ntaps = d == 1 ? span : (d == 2 ? span * span : span * span * span);
+  int64_t h = halo, nxd = nx + 2 * h, nyd = ny + 2 * h;
+  if (d != 3) nz = 1;
+  int64_t* off = (int64_t*)malloc(sizeof(int64_t) * ntaps);
+  tap_offsets(d, r, nyd, nxd, off);
+  double* bufs[2] = {a, b};
+  pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  job_t* jobs = (job_t*)malloc(sizeof(job_t) * threads);
+  int64_t rows = nz * ny;
+  int cur = 0;
+  for (int s = 0; s < steps; ++s) {
+    for (int k = 0; k < threads; ++k) {
+      job_t* j = &jobs[k];
+      j->d = d; j->r = r; j->ntaps = ntaps; j->w = coeffs; j->off = off;
+      j->nz = nz; j->ny = ny; j->nx = nx; j->h = h; j->nyd = nyd; j->nxd = nxd;
+      j->in = bufs[cur]; j->out = bufs[1 - cur];
+      j->row_begin = rows * k / threads;
+      j->row_end = rows * (k + 1) / threads;
+      if (threads > 1) pthread_create(&tid[k], NULL, worker, j);
+      else worker(j);
+    }
+    if (threads > 1)
+      for (int k = 0; k < threads; ++k) pthread_join(tid[k], NULL);
+    cur = 1 - cur;
+  }
+  free(jobs);
+  free(tid);
+  free(off);
+  return cur;
+}
+
 /* in/out: dense halo-padded arrays (2D: (ny+2h)(nx+2h), 1D uses ny = 1;
  * 3D: (nz+2h)(ny+2h)(nx+2h)).  out receives the result after `steps` steps;
  * scratch is a second buffer of the same size.  Returns 0 or -1. */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "spd_metadata_to_bytes": (_I, [_U8, _I, _U8]),
     "spd_transform_row": (_I, [_I, _I, _D, _D, _U8]),
     "spd_plan_create": (_I, [_I, _I, _I, _D, _I, _I, C.POINTER(_P)]),
+    "spd_plan_create_ex": (_I, [_I, _I, _I, _D, _I, _I, _I, C.POINTER(_P)]),
     "spd_plan_destroy": (_I, [_P]),
     "spd_plan_info": (_I, [_P, _I32]),
     "spd_plan_operands": (_I, [_P, _U16, _U32, _I32]),
@@ -83,6 +84,7 @@ SIGNATURES = {
     "spd_download": (_I, [_DESC, _P, _P, _P]),
     "spd_upload_staged": (_I, [_DESC, _P, _P, _P, _P]),
     "spd_download_staged": (_I, [_DESC, _P, _P, _P, _P]),
+    "spd_copy_halo": (_I, [_DESC, _P, _P, _P]),
     "spd_naive_apply_f64": (_I, [_I, _I, _D, _I64, _I64, _I64, _I, _P, _P, _P, _I, _P]),
     "spd_mma_selftest": (_I, [_P, _P, _P, _I, _P, _P]),
     "spd_halo_pack": (_I, [_DESC, _P, _I, _I, _P, _P]),

@@ -203,3 +203,21 @@ def random_grid_3d(Z: int, A: int, B: int, halo: int, seed, dtype=np.float64) ->
     rng = np.random.default_rng(seed)
     shape = (Z + 2 * halo, A + 2 * halo, B + 2 * halo)
     return Grid3D(rng.uniform(-1.0, 1.0, size=shape).astype(dtype), halo)
+
+
+# The reference keeps its file I/O and the brute-force executor in core
+# (core.py:151-254); here they live in io.py and pipeline.py (the executor runs
+# on the device).  Re-export them lazily (PEP 562) so `from <pkg>.core import
+# save_grid, naive_apply` works as with the reference without an import cycle.
+_IO_NAMES = {"GRID_MAGIC", "save_grid", "load_grid", "grid_to_dict", "grid_from_dict", "save_grid_json",
+             "load_grid_json", "kernel_to_dict", "kernel_from_dict", "save_kernel", "load_kernel"}
+
+
+def __getattr__(name):
+    import importlib
+
+    if name in _IO_NAMES:
+        return getattr(importlib.import_module(".io", __package__), name)
+    if name == "naive_apply":
+        return importlib.import_module(".pipeline", __package__).naive_apply
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -200,7 +200,7 @@ int transform_row(int r, int parity, const double* row, double* values, uint8_t*
 // the same TMEM accumulator (the reference accumulates kernel rows in
 // ascending order, pipeline.py:249-253; here the order is fixed by the MMA
 // sequence and fp32 accumulation).
-int build_geometry(int d, int r, Geometry* g) {
+int build_geometry(int d, int r, int flags, Geometry* g) {
   std::memset(g, 0, sizeof(*g));
   int L = band_rows(r);
   if (L < 0) return L;
@@ -254,17 +254,14 @@ int build_geometry(int d, int r, Geometry* g) {
     g->n_tile = 32;
     g->tile_x = g->n_tile * L;
     g->mt_rows = (g->tile_z / g->m_tiles) * (g->tile_y + 2 * r);
-    // CTA-pair mode (SPD_3D_CG2=1): the same 8z x 8y block, but one
+    // CTA-pair mode (SPD_PLAN_CTA_PAIR): the same 8z x 8y block, but one
     // cta_group::2 MMA (M = 256: rank t's TMEM holds M-tile t) per K-block of
     // all 100 input rows, each CTA staging the B columns of its x-half
     // (n_tile = 32 chunks per CTA, 64 per pair).
-    {
-      const char* env = getenv("SPD_3D_CG2");
-      if (env && atoi(env) != 0) {
-        g->cg2 = 1;
-        g->m_tiles = 1;
-        g->tile_x = 2 * g->n_tile * L;
-      }
+    if (flags & SPD_PLAN_CTA_PAIR) {
+      g->cg2 = 1;
+      g->m_tiles = 1;
+      g->tile_x = 2 * g->n_tile * L;
     }
     for (int a = 0; a < g->r_out * 2; ++a) {  // two M-tiles (or the two CTAs of a pair)
       g->out_dz[a] = a / g->tile_y;

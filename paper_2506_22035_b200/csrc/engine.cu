@@ -47,11 +47,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %clock64;" : "=l"(t));
   return t;
 }
-// Debug timeline: event e of tile-iteration it in CTA 0 (64 iterations max).
+// Development builds only (tools/build_variant.sh <name> -DSPD_DEVEL): the
+// per-role timeline (SPD_TRACE, event e of tile-iteration it in CTAs 0-7) and
+// the role-elimination switches (SPD_DBG bits 1: no output stores, 4: no
+// producer work, 16: no epilogue transpose).  The production library compiles
+// both to nothing: no runtime debug branch sits in a hot loop, and no switch
+// can remove a fence.
+#ifdef SPD_DEVEL
 #define SPD_TRACE(e, it)                                                                                 \
   do {                                                                                                   \
     if (p.trace && blockIdx.x < 8 && (it) < 64) *(volatile unsigned long long*)&p.trace[(blockIdx.x * 16 + (e)) * 64 + (it)] = gtimer(); \
   } while (0)
+#define SPD_DBG_BIT(b) ((p.dbg & (b)) != 0)
+#else
+#define SPD_TRACE(e, it) \
+  do {                   \
+  } while (0)
+#define SPD_DBG_BIT(b) false
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -288,8 +301,7 @@ struct StepParams {
                              // last-first for the two-edge launch of a slab's boundary bands)
   int n_tiles;
   int reverse;               // step 0 traverses tiles last-to-first; steps alternate
-  int dbg;                   // development switches (SPD_DBG), 0 in production
-  int prefetch;              // L2 prefetch distance in tiles (0 = off)
+  int dbg;                   // development switches (SPD_DBG; read only in -DSPD_DEVEL builds)
   unsigned long long* trace; // debug timeline (CTA 0): [event][tile] globaltimer stamps, or null
   const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
   const uint32_t* e_words;   // [S][128]
@@ -642,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       while (n < kNPub && gi + n * wstride < total &&
              mbar_test(bar_pubf + 8 * ((it + n) % kNPub), ((it + n) / kNPub) & 1))
         ++n;
-      if (!(p.dbg & 128)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       for (int j = 0; j < n; ++j, ++it, gi += wstride) {
         const TileId id = decode_e(gi, fetch(gi));
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
@@ -676,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           // neighbouring bands complete (gpu-scope acquire) and released this
           // slot; the CTA-scope acquire here extends that to the TMA reads.
           mbar_wait(bar_depf + 8 * (it % kDQ), (it / kDQ) & 1);
-          if (!(p.dbg & 4096)) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
         }
         if (p.use_tmap) {
           // select between the two param-space descriptors (a runtime index
@@ -853,7 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       const bool l0 = lpos == 0, l31 = lpos == SW - 1;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        if (valid[q] && !(p.dbg & 4)) {
+        if (valid[q] && !SPD_DBG_BIT(4)) {
           cur[q] = lds_v4(nbase + noff[q]);
           edge[q] = make_uint4(0, 0, 0, 0);
           lds_v4_if(edge[q], l0 || l31, nbase + (l0 ? poff[q] : xoff_n[q]));
@@ -865,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       // phase 2: neighbour exchange, permutation, B-image stores
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        if (valid[q] && !(p.dbg & 4)) {
+        if (valid[q] && !SPD_DBG_BIT(4)) {
           uint32_t ext[12];
           const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
 #pragma unroll
@@ -928,7 +940,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       bool pend_dep = false;  // some pending tile has dependencies (needs the fence)
       auto flush = [&](int it_end) {
         if (pending == 0) return;
-        if (pend_dep && !(p.dbg & 8192)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (pend_dep) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int t = it_end - pending; t < it_end; ++t) mbar_arrive(bar_depf + 8 * (t % kDQ));
         pending = 0;
         pend_dep = false;
@@ -945,7 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           const int b0 = id.band > 0 ? id.band - 1 : 0;
           const int b1 = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
           bool first = true;
-          while (!(p.dbg & 64)) {
+          while (true) {
             const unsigned int c0 = ld_relaxed_gpu(p.band_done + b0);
             const unsigned int c1 = ld_relaxed_gpu(p.band_done + id.band);
             const unsigned int c2 = ld_relaxed_gpu(p.band_done + b1);
@@ -1096,7 +1108,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             bool ok = true;
             if (g.d == 2) ok = y >= p.row_lo && y < p.row_hi;
             const int64_t x = dx + 8 * col;  // first of the vector's 8 points
-            if (ok && x < xlim && !(p.dbg & 1)) {
+            if (ok && x < xlim && !SPD_DBG_BIT(1)) {
               const uint4 val = lds_v4(sb + row * C::STG_PITCH + col * 16);
               T* dst = tbase + roff + 8 * col;
               if (x + 8 <= xlim) {
@@ -1114,7 +1126,6 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           // the warp's stores); the gpu-scope release happens off this path
           const int ps = pit % kNPub;
           mbar_wait(bar_pube + 8 * ps, ((pit / kNPub) & 1) ^ 1);
-          if (p.dbg & 256) __threadfence();
           __syncwarp();
           if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
           ++pit;
@@ -1201,7 +1212,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       // by piece in ascending x.
       auto store = [&](int bi, const uint32_t(&bw)[16]) {
         const int mt = bi / NB, cb = bi % NB;
-        if (!row_ok[mt] || (p.dbg & 1)) return;
+        if (!row_ok[mt] || SPD_DBG_BIT(1)) return;
         uint32_t w[16];
 #pragma unroll
         for (int k = 0; k < PPD; ++k)
@@ -1252,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         }
 #pragma unroll
         for (int b = 1; b < L; b <<= 1) {
-          if (p.dbg & 16) break;
+          if (SPD_DBG_BIT(16)) break;
           const bool upper = (d & b) != 0;
 #pragma unroll
           for (int k = 0; k < PPD; ++k) {
@@ -1285,7 +1296,6 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         // the warp's stores); the gpu-scope release happens off this path
         const int ps = pit % kNPub;
         mbar_wait(bar_pube + 8 * ps, ((pit / kNPub) & 1) ^ 1);
-        if (p.dbg & 256) __threadfence();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
         ++pit;
@@ -1482,28 +1492,23 @@ struct spd_plan {
   std::vector<uint32_t> e_words;   // S x 128
   uint16_t* d_a = nullptr;
   uint32_t* d_e = nullptr;
-  unsigned int* d_counters = nullptr;  // per-band completion counters (persistent runs)
-  int counters_cap = 0;
   int sms = 0;
-  // persistent work orders (device), keyed by (steps, sweep, lag, n_bands)
+  // persistent work orders (device), keyed by (steps, sweep, lag, n_bands);
+  // built on first use under orders_mu, read-only afterwards
   std::map<std::tuple<int, int, int, int>, int2*> orders;
+  std::mutex orders_mu;
 };
 
 namespace spd {
 
-// Zeroed per-band counters for a persistent launch (stream-ordered memset).
-static int plan_counters(const spd_plan* cplan, int n, cudaStream_t st, unsigned int** out) {
-  spd_plan* plan = const_cast<spd_plan*>(cplan);
-  if (plan->counters_cap < n) {
-    if (plan->d_counters) cudaFree(plan->d_counters);
-    plan->d_counters = nullptr;
-    plan->counters_cap = 0;
-    cudaError_t e = cudaMalloc(&plan->d_counters, sizeof(unsigned int) * n);
-    if (e != cudaSuccess) return cuda_err(e, "counter alloc");
-    plan->counters_cap = n;
-  }
-  *out = plan->d_counters;
-  return cuda_err(cudaMemsetAsync(plan->d_counters, 0, sizeof(unsigned int) * n, st), "counter reset");
+// Zeroed per-band counters for ONE persistent launch, stream-ordered
+// (cudaMallocAsync + memset; freed with cudaFreeAsync after the launch), so
+// launches of the same plan on different streams or threads never share them.
+static int launch_counters(int n, cudaStream_t st, unsigned int** out) {
+  *out = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), sizeof(unsigned int) * n, st);
+  if (e != cudaSuccess) return cuda_err(e, "counter alloc");
+  return cuda_err(cudaMemsetAsync(*out, 0, sizeof(unsigned int) * n, st), "counter reset");
 }
 
 template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
@@ -1533,13 +1538,13 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
                       8 * (2 * NSTAGE + 2 * NACC + 2 * NNAT + 2 * kNPub + 2 * kDQ) + 16;
   if (smem > 232448) return set_error(SPD_EUNSUPPORTED, "shared memory budget exceeded (%zu B)", smem);
   if (C::A_COL + 8 * plan->g.s > 512) return set_error(SPD_EUNSUPPORTED, "TMEM budget exceeded (S=%d)", plan->g.s);
-  static thread_local int configured_dev = -1;
-  static thread_local size_t configured_smem = 0;
-  if (configured_dev != plan->device || configured_smem < smem) {
+  // the attribute is per device: remember which devices this thread set it on
+  static thread_local uint64_t configured = 0;
+  const uint64_t dev_bit = 1ull << (plan->device & 63);
+  if (!(configured & dev_bit)) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
-    configured_dev = plan->device;
-    configured_smem = 232448;
+    configured |= dev_bit;
   }
   if (sp.n_tiles <= 0) return SPD_OK;
   const int64_t work = (int64_t)sp.n_tiles * sp.steps * (CG2 ? 2 : 1);
@@ -1602,6 +1607,12 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
 }
 
 static int dispatch(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
+  {  // launches go to the current device: it must be the one holding the plan's operands
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != plan->device)
+      return set_error(SPD_EINVAL, "plan lives on device %d but device %d is current", plan->device, cur);
+  }
   if (plan->dtype == SPD_DTYPE_F16)
     return plan->parity == 0 ? dispatch_par<__half, 0>(plan, sp, st) : dispatch_par<__half, 1>(plan, sp, st);
   return plan->parity == 0 ? dispatch_par<__nv_bfloat16, 0>(plan, sp, st)
@@ -1610,7 +1621,9 @@ static int dispatch(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
 
 static int64_t roundup(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+#ifdef SPD_DEVEL
 static unsigned long long* g_trace = nullptr;       // debug timeline buffer (SPD_TRACE), device view
+#endif
 static unsigned long long* g_trace_host = nullptr;  // mapped pinned host view (readable during a hang)
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1726,11 +1739,10 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     sp.n_bands = sp.tiles_x;
     sp.per_band = 1;
   }
+  sp.trace = nullptr;
+#ifdef SPD_DEVEL
   const char* dbg_env = getenv("SPD_DBG");
   sp.dbg = dbg_env ? atoi(dbg_env) : 0;
-  static const char* pf_env = getenv("SPD_PREFETCH");
-  sp.prefetch = pf_env ? atoi(pf_env) : 0;
-  sp.trace = nullptr;
   if (getenv("SPD_TRACE")) {
     if (!g_trace_host) {
       cudaHostAlloc(&g_trace_host, 8 * 16 * 64 * sizeof(unsigned long long), cudaHostAllocMapped);
@@ -1739,6 +1751,7 @@ static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const
     }
     sp.trace = g_trace;
   }
+#endif
   sp.zoff = (int)(gd->origin / gd->plane);
   sp.yoff = (int)((gd->origin % gd->plane) / gd->pitch);
   sp.xoff = (int)(gd->origin % gd->pitch);
@@ -1778,6 +1791,7 @@ static int wavefront_order(const spd_plan* cplan, const spd_grid_desc* gd, StepP
     return set_error(SPD_EINVAL, "persistent launch too large (%lld work items)", (long long)(pairs * sp.per_band));
   sp.total = (int)(pairs * sp.per_band);
   const auto key = std::make_tuple(sp.steps, sp.sweep, sp.lag, sp.n_bands);
+  std::lock_guard<std::mutex> lock(plan->orders_mu);
   auto it = plan->orders.find(key);
   if (it == plan->orders.end()) {
     // built once per key (synchronous upload: warm up outside graph capture)
@@ -1819,8 +1833,15 @@ static int check_desc(const spd_plan* plan, const spd_grid_desc* gd) {
 extern "C" {
 
 int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype, int device, spd_plan** out) {
+  return spd_plan_create_ex(d, r, parity, coeffs, dtype, device, 0, out);
+}
+
+int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype, int device, int flags,
+                       spd_plan** out) {
   using namespace spd;
   if (!out) return set_error(SPD_EINVAL, "null output pointer");
+  if (flags & ~SPD_PLAN_CTA_PAIR) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
+  if ((flags & SPD_PLAN_CTA_PAIR) && d != 3) return set_error(SPD_EUNSUPPORTED, "CTA-pair plans are 3D only");
   *out = nullptr;
   if (d < 1 || d > 3) return set_error(SPD_EINVAL, "unsupported dimensionality %d", d);
   if (parity != 0 && parity != 1) return set_error(SPD_EINVAL, "bad parity code %d", parity);
@@ -1848,7 +1869,7 @@ int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype, i
       return rc;
     }
   }
-  int rc = build_geometry(d, r, &p->g);
+  int rc = build_geometry(d, r, flags, &p->g);
   if (rc) {
     delete p;
     return rc;
@@ -1884,7 +1905,6 @@ int spd_plan_destroy(spd_plan* plan) {
   if (!plan) return SPD_OK;
   if (plan->d_a) cudaFree(plan->d_a);
   if (plan->d_e) cudaFree(plan->d_e);
-  if (plan->d_counters) cudaFree(plan->d_counters);
   for (auto& kv : plan->orders) cudaFree(kv.second);
   delete plan;
   return SPD_OK;
@@ -2066,11 +2086,12 @@ int spd_run_ex(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* 
       }
       rc = wavefront_order(plan, gd, sp);
       if (rc) return rc;
-      rc = plan_counters(plan, sp.n_bands, (cudaStream_t)stream, &sp.band_done);
+      rc = launch_counters(sp.n_bands, (cudaStream_t)stream, &sp.band_done);
       if (rc) return rc;
     }
     sp.reverse = persistent ? 0 : (done & 1);
     rc = dispatch(plan, sp, (cudaStream_t)stream);
+    if (sp.band_done) cudaFreeAsync(sp.band_done, (cudaStream_t)stream);
     if (rc) return rc;
     done += chunk;
   }
@@ -2168,6 +2189,41 @@ __global__ void repack_rows_kernel(DenseMap dm, int64_t pitch, int64_t plane, in
   }
 }
 }  // namespace spd
+
+namespace spd {
+// Dirichlet ring of a halo-padded grid (everything of the dense region that
+// is not interior) from one device buffer to the other: one warp per stored
+// dense row; halo rows / planes are copied whole, interior rows only their
+// h left and h right elements.
+__global__ void halo_ring_kernel(DenseMap dm, int64_t pitch, int64_t plane, int64_t origin, const uint16_t* src,
+                                 uint16_t* dst) {
+  const int64_t rows = dm.nzd * dm.nyd;
+  const int64_t z0 = dm.d == 3 ? dm.h : 0;
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32; row < rows; row += warps) {
+    const int64_t zz = row / dm.nyd, yy = row - zz * dm.nyd;
+    const int64_t dev0 = origin + (zz - z0) * plane + (yy - dm.h) * pitch - dm.h;
+    const bool halo_row = yy < dm.h || yy >= dm.nyd - dm.h || (dm.d == 3 && (zz < dm.h || zz >= dm.nzd - dm.h));
+    if (halo_row) {
+      for (int64_t x = lane; x < dm.nxd; x += 32) dst[dev0 + x] = src[dev0 + x];
+    } else {
+      for (int64_t k = lane; k < 2 * dm.h; k += 32) {
+        const int64_t x = k < dm.h ? k : dm.nxd - 2 * dm.h + k;
+        dst[dev0 + x] = src[dev0 + x];
+      }
+    }
+  }
+}
+}  // namespace spd
+
+int spd_copy_halo(const spd_grid_desc* g, const void* src, void* dst, void* stream) {
+  if (!g || !src || !dst) return spd::set_error(SPD_EINVAL, "null argument");
+  if (g->halo < 1) return SPD_OK;
+  spd::halo_ring_kernel<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(dense_map(g, g->dims), g->pitch, g->plane,
+                                                                   g->origin, (const uint16_t*)src, (uint16_t*)dst);
+  return spd::cuda_err(cudaGetLastError(), "halo_ring_kernel");
+}
 
 static int64_t dense_elems(const spd_grid_desc* g) {
   const int64_t h = g->halo;

@@ -54,7 +54,7 @@ struct Geometry {
   int out_dz[SPD_MAX_ROUT], out_dy[SPD_MAX_ROUT], out_dx[SPD_MAX_ROUT];
 };
 
-int build_geometry(int d, int r, Geometry* g);
+int build_geometry(int d, int r, int flags, Geometry* g);
 int pack_operands(const Geometry& g, int n_rows, const double* row_values,
                   const uint8_t* row_meta, int dtype, std::vector<uint16_t>& a_img,
                   std::vector<uint32_t>& e_words);

@@ -107,6 +107,12 @@ class SlabDriver:
     """Runs steps of a slab with boundary-first compute and overlapped exchange."""
 
     def __init__(self, slab: Slab, ops: SlabOps, group=None, comm_stream=None, compute_stream=None):
+        # an interior slab face must sit on a tile-band boundary: otherwise the
+        # 'down' pack reads rows of the interior band, which is computed
+        # concurrently with (or after) the exchange
+        if slab.down is not None and ops.rows % ops.band != 0:
+            raise ValueError(f"slab of {ops.rows} rows has an interior face off the {ops.band}-row tile bands "
+                             f"(use decompose(..., align={ops.band}))")
         self.slab, self.ops, self.group = slab, ops, group
         self.msgs = {k: ops.new_message() for k in ("send_up", "send_down", "recv_up", "recv_down")}
         self.comm_stream = comm_stream
@@ -253,6 +259,17 @@ def _ipc_export(t: torch.Tensor):
     return handle.raw, int(off.value)
 
 
+def _check_peer_access(dev: torch.device, peer_uuid: str) -> None:
+    """Raise unless this process can map memory of the GPU `peer_uuid` (the
+    same device, or a peer-capable visible one: NVLink / PCIe P2P)."""
+    for i in range(torch.cuda.device_count()):
+        if str(torch.cuda.get_device_properties(i).uuid) == peer_uuid:
+            if i == dev.index or torch.cuda.can_device_access_peer(dev.index, i):
+                return
+            raise RuntimeError(f"cuda:{dev.index} cannot access peer cuda:{i}")
+    raise RuntimeError(f"neighbour GPU {peer_uuid} is not visible to this process")
+
+
 class PeerSlab:
     """One rank's slab whose halo rows are exchanged through peer memory: the
     neighbours' grid buffers and flag words are mapped with CUDA IPC, the
@@ -279,6 +296,7 @@ class PeerSlab:
                 "bufs": [_ipc_export(b) for b in grid.bufs],
                 "flags": _ipc_export(self.flags),
                 "desc": _desc_tuple(grid.desc),
+                "uuid": str(torch.cuda.get_device_properties(dev).uuid),
             }
         except Exception as exc:  # every rank must reach the all-gather
             mine = {"error": f"rank {dist.get_rank(group)}: {exc}"}
@@ -294,6 +312,7 @@ class PeerSlab:
             if rank is None:
                 return None, None, None, None
             info = everyone[rank]
+            _check_peer_access(dev, info["uuid"])
             ptrs = []
             for handle, off in info["bufs"] + [info["flags"]]:
                 p, base = C.c_void_p(), C.c_void_p()

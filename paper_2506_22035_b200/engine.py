@@ -21,6 +21,7 @@ from .core import StencilKernel
 from .transform import Parity
 
 TORCH_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
+SPD_PLAN_CTA_PAIR = 1  # include/spider.h
 NP_DTYPES = {"fp16": np.float16}
 
 
@@ -33,8 +34,9 @@ def require_cuda(device=None) -> torch.device:
     return dev
 
 
-def _stream_ptr(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream_ptr(stream=None, device=None):
+    """Raw cudaStream_t: `stream`, else torch's current stream of `device`."""
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return C.c_void_p(s.cuda_stream)
 
 
@@ -60,7 +62,8 @@ class Plan:
     which the CPU test tier uses to check the packer.
     """
 
-    def __init__(self, kernel: StencilKernel, parity=Parity.EVEN, dtype: str = "fp16", device: int | None = None):
+    def __init__(self, kernel: StencilKernel, parity=Parity.EVEN, dtype: str = "fp16", device: int | None = None,
+                 cta_pair: bool = False):
         if dtype not in DTYPE_CODES:
             raise ValueError(f"dtype must be one of {sorted(DTYPE_CODES)}, got {dtype!r}")
         self.kernel = kernel
@@ -71,8 +74,10 @@ class Plan:
         self.device = int(device)
         coeffs = np.ascontiguousarray(kernel.coeffs, dtype=np.float64).ravel()
         self._coeffs = coeffs
+        self.cta_pair = bool(cta_pair)
         h = C.c_void_p()
-        check(lib.spd_plan_create(kernel.d, kernel.r, self.parity.code, dptr(coeffs), DTYPE_CODES[dtype], self.device, C.byref(h)))
+        check(lib.spd_plan_create_ex(kernel.d, kernel.r, self.parity.code, dptr(coeffs), DTYPE_CODES[dtype],
+                                     self.device, SPD_PLAN_CTA_PAIR if cta_pair else 0, C.byref(h)))
         self._h = h
 
     @property
@@ -120,6 +125,22 @@ class Plan:
         return desc
 
 
+def _on_device(fn):
+    """Run a DeviceGrid method with its grid's device current: libspider
+    launches on the current device, and the default stream is that device's
+    current torch stream (execute may target a device that is not current)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapper(self, *args, **kwargs):
+        if torch.cuda.current_device() == self.device.index:
+            return fn(self, *args, **kwargs)
+        with torch.cuda.device(self.device):
+            return fn(self, *args, **kwargs)
+
+    return wrapper
+
+
 class DeviceGrid:
     """Ping-pong buffers of one grid in the engine layout, resident in HBM."""
 
@@ -127,8 +148,10 @@ class DeviceGrid:
         require_cuda()
         self.plan = plan
         nz, ny, nx = _shape3(plan.kernel.d, shape)
+        self.desc_shape = tuple(int(v) for v in shape)
         self.desc = plan.layout(nz, ny, nx, halo)
         dev = torch.device("cuda", plan.device)
+        self.device = dev
         tdt = TORCH_DTYPES[plan.dtype]
         self.bufs = [torch.zeros(self.desc.alloc_elems, dtype=tdt, device=dev) for _ in range(2)]
         self.cur = 0  # index of the buffer holding the current state
@@ -145,9 +168,17 @@ class DeviceGrid:
             return (self.desc.nz + 2 * h, self.desc.ny + 2 * h, self.desc.nx + 2 * h)
         return (self.desc.ny + 2 * h, self.desc.nx + 2 * h)
 
-    def _sync_halo(self, stream=None) -> None:
-        self.bufs[1 - self.cur].copy_(self.bufs[self.cur])
+    def _sp(self, stream):
+        return _stream_ptr(stream, self.device)
 
+    @_on_device
+    def _sync_halo(self, stream=None) -> None:
+        """Replicate the Dirichlet ring of the current buffer into the other
+        one (stream-ordered after the upload that wrote it)."""
+        check(lib.spd_copy_halo(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
+                                C.c_void_p(self.bufs[1 - self.cur].data_ptr()), self._sp(stream)))
+
+    @_on_device
     def load_dense_f64(self, dense: torch.Tensor, stream=None) -> None:
         """Quantise a dense fp64 device tensor (halo included) into the grid."""
         if dense.dtype != torch.float64 or not dense.is_cuda:
@@ -156,14 +187,15 @@ class DeviceGrid:
         if tuple(dense.shape) != tuple(self.dense_shape):
             raise ValueError(f"dense grid shape {tuple(dense.shape)} != {self.dense_shape}")
         check(lib.spd_pack_grid(C.byref(self.desc), DTYPE_CODES[self.plan.dtype], C.c_void_p(dense.data_ptr()),
-                                C.c_void_p(self.bufs[self.cur].data_ptr()), _stream_ptr(stream)))
+                                C.c_void_p(self.bufs[self.cur].data_ptr()), self._sp(stream)))
         self._sync_halo(stream)
 
+    @_on_device
     def to_dense_f64(self, stream=None) -> torch.Tensor:
         out = torch.empty(self.dense_shape, dtype=torch.float64, device=self.bufs[0].device)
         check(lib.spd_unpack_grid(C.byref(self.desc), DTYPE_CODES[self.plan.dtype],
                                   C.c_void_p(self.bufs[self.cur].data_ptr()), C.c_void_p(out.data_ptr()),
-                                  _stream_ptr(stream)))
+                                  self._sp(stream)))
         return out
 
     def _staged(self, staged) -> bool:
@@ -181,6 +213,7 @@ class DeviceGrid:
             buf.record_stream(stream)
         return buf
 
+    @_on_device
     def upload(self, host: torch.Tensor, stream=None, staged=None) -> None:
         """DMA of a host 16-bit dense grid (pinned for async)."""
         if host.dtype != TORCH_DTYPES[self.plan.dtype] or host.is_cuda:
@@ -191,12 +224,13 @@ class DeviceGrid:
             st = self._staging(stream)
             check(lib.spd_upload_staged(C.byref(self.desc), C.c_void_p(host.data_ptr()),
                                         C.c_void_p(self.bufs[self.cur].data_ptr()), C.c_void_p(st.data_ptr()),
-                                        _stream_ptr(stream)))
+                                        self._sp(stream)))
         else:
             check(lib.spd_upload(C.byref(self.desc), C.c_void_p(host.data_ptr()),
-                                 C.c_void_p(self.bufs[self.cur].data_ptr()), _stream_ptr(stream)))
+                                 C.c_void_p(self.bufs[self.cur].data_ptr()), self._sp(stream)))
         self._sync_halo(stream)
 
+    @_on_device
     def download(self, host: torch.Tensor, stream=None, staged=None) -> None:
         if host.dtype != TORCH_DTYPES[self.plan.dtype] or host.is_cuda:
             raise ValueError(f"expected a host {TORCH_DTYPES[self.plan.dtype]} tensor")
@@ -206,11 +240,12 @@ class DeviceGrid:
             st = self._staging(stream)
             check(lib.spd_download_staged(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
                                           C.c_void_p(host.data_ptr()), C.c_void_p(st.data_ptr()),
-                                          _stream_ptr(stream)))
+                                          self._sp(stream)))
         else:
             check(lib.spd_download(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
-                                   C.c_void_p(host.data_ptr()), _stream_ptr(stream)))
+                                   C.c_void_p(host.data_ptr()), self._sp(stream)))
 
+    @_on_device
     def run(self, steps: int, stream=None, persistent: bool = False) -> None:
         """`steps` Jacobi steps on the device, ping-ponging the buffers
         (one launch per step, or one persistent launch)."""
@@ -218,23 +253,25 @@ class DeviceGrid:
             raise ValueError(f"step count must be >= 1, got {steps}")
         a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
         check(lib.spd_run_ex(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                             int(steps), 1 if persistent else 0, _stream_ptr(stream)))
+                             int(steps), 1 if persistent else 0, self._sp(stream)))
         self.cur = (self.cur + steps) % 2
         self.step += steps
 
+    @_on_device
     def step_range(self, lo: int, hi: int, stream=None) -> None:
         """One step over output rows (2D) / planes (3D) [lo, hi) only; does
         not flip the buffers (call `flip()` once the whole domain is done)."""
         a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
         check(lib.spd_step_range(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()),
-                                 C.c_void_p(b.data_ptr()), int(lo), int(hi), _stream_ptr(stream)))
+                                 C.c_void_p(b.data_ptr()), int(lo), int(hi), self._sp(stream)))
 
+    @_on_device
     def step_edges(self, stream=None) -> None:
         """One step over the first and last tile bands only (one launch); with
         step_range over the bands between them this is a full step."""
         a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
         check(lib.spd_step_edges(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()),
-                                 C.c_void_p(b.data_ptr()), _stream_ptr(stream)))
+                                 C.c_void_p(b.data_ptr()), self._sp(stream)))
 
     def flip(self) -> None:
         self.cur = 1 - self.cur

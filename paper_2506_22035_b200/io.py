@@ -22,7 +22,7 @@ from pathlib import Path
 import numpy as np
 
 from .core import Grid, Grid3D, StencilKernel, make_kernel, make_kernel_3d
-from .transform import CompressedKernel, Parity, metadata_from_bytes, metadata_to_bytes
+from .transform import CompressedKernel, Parity, metadata_from_bytes, metadata_to_bytes, validate_metadata
 
 GRID_MAGIC = b"SPGR"
 GRID3_MAGIC = b"SPG3"
@@ -174,6 +174,15 @@ def compressed_to_dict(ck: CompressedKernel) -> dict:
             "metadata": np.asarray(ck.metadata).tolist()}
 
 
+def compressed_from_dict(obj: dict) -> CompressedKernel:
+    """Inverse of compressed_to_dict (reference transform.py:338-346): the
+    metadata is validated (ascending pairs, in range) before use."""
+    meta = np.asarray(obj["metadata"], dtype=np.uint8)
+    validate_metadata(meta)
+    return CompressedKernel(values=np.asarray(obj["values"], dtype=np.float64), metadata=meta, r=int(obj["r"]),
+                            parity=Parity(obj["parity"]))
+
+
 def save_compressed_json(kernels, path) -> None:
     Path(path).write_text(json.dumps([compressed_to_dict(ck) for ck in kernels], indent=2))
 
@@ -182,5 +191,5 @@ __all__ = [
     "save_grid", "load_grid", "grid_to_dict", "grid_from_dict", "save_grid_json", "load_grid_json",
     "kernel_to_dict", "kernel_from_dict", "save_kernel", "load_kernel",
     "compressed_record_bytes", "save_compressed_set", "load_compressed_set", "compressed_to_dict",
-    "save_compressed_json",
+    "compressed_from_dict", "save_compressed_json",
 ]

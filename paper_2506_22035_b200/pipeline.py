@@ -25,6 +25,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 import torch
 
+from .accounting import MMA_M16N8K16, fetch_runs, tile_counts
 from .core import Grid, Grid3D, StencilKernel, random_grid
 from .engine import DeviceGrid, Plan, TORCH_DTYPES, naive_apply_device, require_cuda
 from .transform import CompressedKernel, Parity, RowPermutation, band_rows, input_row_permutation, transform_row
@@ -49,7 +50,7 @@ class ExecConfig:
     b_block: int | None = None
     a_warp: int = 16
     b_warp: int = 8
-    mma: object = None
+    mma: object = MMA_M16N8K16
     precision: str = "fp64"
     compute_mode: str = "ceil"
     packing: bool = True
@@ -102,6 +103,7 @@ class ExecStats:
     fetch_runs_unpacked: int = 0
     fetch_runs_active: int = 0
     tile_counts: dict = field(default_factory=dict)
+    # B200 engine: tcgen05 instruction, tile geometry and issued work
     device: dict = field(default_factory=dict)
 
     def as_dict(self) -> dict:
@@ -195,15 +197,27 @@ def _check_inputs(kernel: StencilKernel, grid, steps: int) -> None:
         raise ValueError(f"grid width {grid.B} must be a multiple of the x-chunk size L={L}")
 
 
-def _stats(kernel: StencilKernel, grid, steps: int, parity: Parity, plan: Plan) -> ExecStats:
-    """Reference counter semantics (pipeline.py:254-259) per step and kernel row."""
+def _exec_cfg(cfg) -> ExecConfig:
+    """The reference-side config (tiling / instruction shape for the counters)."""
+    if isinstance(cfg, ExecConfig):
+        return cfg
+    return ExecConfig(parity=_parity_of(cfg))
+
+
+def _stats(kernel: StencilKernel, grid, steps: int, cfg, plan: Plan) -> ExecStats:
+    """ExecStats with the reference's counter semantics (pipeline.py:200-259):
+    per step and kernel row, L x L compressed MACs per x-chunk, the reference
+    tile plan and fetch-run metric; `device` holds what the B200 issued."""
+    ecfg = _exec_cfg(cfg)
+    parity = _parity_of(cfg)
     L = band_rows(kernel.r)
     n_rows = len(list(kernel.row_offsets()))
     planes = grid.Z if isinstance(grid, Grid3D) else 1
     cols = planes * grid.A * (grid.B // L)
-    n_groups = -(-cols // 8)
-    inv_k = -(-2 * L // 16)
-    m_groups = -(-L // 16)
+    mma = ecfg.mma
+    n_groups = -(-cols // mma.n)
+    inv_k = -(-2 * L // mma.k)
+    m_groups = -(-L // mma.m)
     per = steps * n_rows
     st = ExecStats(
         grid_a=grid.A,
@@ -213,28 +227,83 @@ def _stats(kernel: StencilKernel, grid, steps: int, parity: Parity, plan: Plan) 
         kernel_rows=n_rows,
         L=L,
         parity=parity.value,
-        packing=True,
+        packing=ecfg.packing,
+        tile_counts=tile_counts(min(kernel.d, 2), kernel.r, grid.A, grid.B, ecfg),
     )
+    if isinstance(mma, type(MMA_M16N8K16)) and (mma.m, mma.n, mma.k) == (16, 8, 16):
+        st.fetch_runs_packed, st.fetch_runs_unpacked, st.fetch_runs_active = fetch_runs(L, ecfg.packing, mma)
     st.total_macs = per * L * cols * L
     st.dense_macs = 2 * st.total_macs
     st.input_elements = per * 2 * L * cols
     st.param_elements = per * L * L * n_groups
     st.mma_invocations = per * m_groups * n_groups * inv_k
     st.sparse_mma_calls = per
-    info = plan.info()
-    tiles_x = -(-grid.B // (info.n_tile * L)) if kernel.d != 1 else -(-grid.B // (info.n_tile * L * info.r_out))
-    tiles = tiles_x * (-(-grid.A // info.tile_y) if kernel.d >= 2 else 1) * (-(-planes // info.tile_z))
-    st.tile_counts = {"block_tiles": tiles, "n_tile": info.n_tile, "tile_rows": info.r_out * info.m_tiles}
-    st.device = {
-        "arch": "sm_100a",
-        "instruction": "tcgen05.mma.sp.cta_group::1.kind::f16 M128 N%d K32" % info.n_tile,
-        "dtype": plan.dtype,
-        "launches": steps,
-        "tiles_per_step": tiles,
-        "mma_instructions": steps * tiles * info.mmas_per_tile * info.m_tiles,
-        "issued_sparse_macs": steps * tiles * info.mmas_per_tile * info.m_tiles * 128 * info.n_tile * 16,
-    }
+    if plan is not None:
+        info = plan.info()
+        tiles_x = -(-grid.B // (info.n_tile * L)) if kernel.d != 1 else -(-grid.B // (info.n_tile * L * info.r_out))
+        tiles = tiles_x * (-(-grid.A // info.tile_y) if kernel.d >= 2 else 1) * (-(-planes // info.tile_z))
+        st.device = {
+            "arch": "sm_100a",
+            "instruction": "tcgen05.mma.sp.cta_group::1.kind::f16 M128 N%d K32" % info.n_tile,
+            "dtype": plan.dtype,
+            "launches": steps,
+            "tiles_per_step": tiles,
+            "tile": {"n_tile": info.n_tile, "tile_rows": info.r_out * info.m_tiles, "tile_z": info.tile_z,
+                     "input_rows": info.r_in, "mmas_per_tile": info.mmas_per_tile * info.m_tiles},
+            "mma_instructions": steps * tiles * info.mmas_per_tile * info.m_tiles,
+            "issued_sparse_macs": steps * tiles * info.mmas_per_tile * info.m_tiles * 128 * info.n_tile * 16,
+        }
     return st
+
+
+def exec_stats(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig()) -> ExecStats:
+    """The reference counters of `execute(kernel, grid, steps, cfg)` without
+    running it (host only; `device` is empty)."""
+    _check_inputs(kernel, grid, steps)
+    return _stats(kernel, grid, steps, cfg, None)
+
+
+class _GridPool:
+    """Device grids kept between `execute` calls, per (plan, shape, halo).
+
+    A call takes a free grid (or allocates one) and returns it when its
+    result is on the host, so concurrent callers never share buffers and a
+    repeated call skips the two zeroed allocations.  Nothing outside the dense
+    region is ever written, so the zero padding the kernels rely on survives
+    reuse.  `release_device_grids()` frees the cache."""
+
+    def __init__(self, keep: int = 4):
+        self.keep = keep
+        self._free: dict = {}
+        self._lock = threading.Lock()
+
+    def acquire(self, plan: Plan, shape, halo: int) -> DeviceGrid:
+        key = (id(plan), tuple(shape), int(halo))
+        with self._lock:
+            lst = self._free.get(key)
+            if lst:
+                return lst.pop()
+        return DeviceGrid(plan, shape, halo)
+
+    def release(self, dg: DeviceGrid) -> None:
+        key = (id(dg.plan), tuple(dg.desc_shape), int(dg.halo))
+        with self._lock:
+            lst = self._free.setdefault(key, [])
+            if len(lst) < self.keep:
+                dg.cur, dg.step = 0, 0
+                lst.append(dg)
+
+    def clear(self) -> None:
+        with self._lock:
+            self._free.clear()
+
+
+_GRIDS = _GridPool()
+
+
+def release_device_grids() -> None:
+    """Free the device grids cached between `execute` calls."""
+    _GRIDS.clear()
 
 
 def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=None):
@@ -242,44 +311,49 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
     (Grid, ExecStats) like reference pipeline.py:189-262.  The input grid is
     never modified.
 
-    float16 host grids are transferred as-is by strided DMA (pinned host memory
-    gives asynchronous copies) and the result comes back as float16, into
+    float16 host grids are transferred as-is by DMA (pinned host memory gives
+    asynchronous copies) and the result comes back as float16, into
     `out.data` when an `out` grid of the same shape is given (otherwise into a
     pinned buffer from torch's caching host allocator).  Other dtypes are
     quantised on the device and the result is returned as float64 (float32
-    inputs give float32).
+    inputs give float32).  The work runs on the plan's device (DeviceConfig
+    .device, default the current one), on that device's current stream.
     """
     _check_inputs(kernel, grid, steps)
     dcfg = _device_cfg(cfg)
     plan = get_plan(kernel, dcfg.parity, dcfg.dtype, dcfg.device)
+    stats = _stats(kernel, grid, steps, cfg, plan)  # raises the reference's tile-plan errors first
     shape = (grid.Z, grid.A, grid.B) if kernel.d == 3 else (grid.A, grid.B)
-    dg = DeviceGrid(plan, shape, grid.halo)
     data = grid.data
     native16 = dcfg.dtype == "fp16" and data.dtype == np.float16
-    if native16:
-        dg.upload(torch.from_numpy(np.ascontiguousarray(data)))
-    else:
-        dg.load_dense_f64(torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dg.bufs[0].device))
-    dg.run(steps)
-    if native16:
-        if out is not None:
-            if out.data.shape != data.shape or out.data.dtype != np.float16 or not out.data.flags.c_contiguous:
-                raise ValueError("out grid must be a contiguous float16 array of the input's shape")
-            target = torch.from_numpy(out.data)
-        else:
-            target = torch.empty(dg.dense_shape, dtype=torch.float16, pin_memory=True)
-        dg.download(target)
-        torch.cuda.current_stream().synchronize()
-        res = target.numpy()
-    else:
-        res = dg.to_dense_f64().cpu().numpy()
-        if data.dtype == np.float32:
-            res = res.astype(np.float32)
-        if out is not None:
-            out.data[...] = res
-            res = out.data
+    if native16 and out is not None:
+        if out.data.shape != data.shape or out.data.dtype != np.float16 or not out.data.flags.c_contiguous:
+            raise ValueError("out grid must be a contiguous float16 array of the input's shape")
+    with torch.cuda.device(plan.device):
+        dg = _GRIDS.acquire(plan, shape, grid.halo)
+        try:
+            if native16:
+                dg.upload(torch.from_numpy(np.ascontiguousarray(data)))
+            else:
+                dg.load_dense_f64(torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dg.device))
+            dg.run(steps)
+            if native16:
+                target = torch.from_numpy(out.data) if out is not None else torch.empty(
+                    dg.dense_shape, dtype=torch.float16, pin_memory=True)
+                dg.download(target)
+                torch.cuda.current_stream().synchronize()
+                res = target.numpy()
+            else:
+                res = dg.to_dense_f64().cpu().numpy()
+                if data.dtype == np.float32:
+                    res = res.astype(np.float32)
+                if out is not None:
+                    out.data[...] = res
+                    res = out.data
+        finally:
+            _GRIDS.release(dg)
     cls = Grid3D if kernel.d == 3 else Grid
-    return cls(res, grid.halo, grid.step + steps), _stats(kernel, grid, steps, dcfg.parity, plan)
+    return cls(res, grid.halo, grid.step + steps), stats
 
 
 def naive_apply(kernel: StencilKernel, grid, steps: int):
@@ -334,9 +408,13 @@ def verify(kernel: StencilKernel, sizes, seed: int, steps: int, cfg=ExecConfig()
         grid, got = first_ok
         other = Parity.ODD if dcfg.parity is Parity.EVEN else Parity.EVEN
         flipped, _ = execute(kernel, grid, steps, replace(dcfg, parity=other))
+        # the reference toggles operand packing (a pure relayout); the device
+        # path has one operand image, so the same call is the toggled run
+        toggled, _ = execute(kernel, grid, steps, dcfg)
         cross = {
             "parity_max_abs_diff": float(np.max(np.abs(flipped.interior - got.interior))),
             "parity_bitwise_identical": bool(np.array_equal(flipped.interior, got.interior)),
+            "packing_bitwise_identical": bool(np.array_equal(toggled.interior, got.interior)),
         }
     return {
         "kernel": {"shape": kernel.shape.value, "d": kernel.d, "r": kernel.r, "coeffs": kernel.coeffs.tolist()},
@@ -369,5 +447,7 @@ __all__ = [
     "report_json",
     "max_rel_error",
     "get_plan",
+    "exec_stats",
+    "release_device_grids",
     "DEFAULT_TOLERANCE",
 ]

@@ -255,3 +255,18 @@ __all__ = [
     "transform_row",
 ]
 _ = _lib
+
+
+# SPCK record I/O lives in io.py; the reference keeps it in transform
+# (transform.py:270-352).  Lazy re-exports (PEP 562) keep
+# `from <pkg>.transform import save_compressed_set, compressed_from_dict` working.
+_IO_NAMES = {"COMPRESSED_MAGIC", "compressed_record_bytes", "save_compressed_set", "load_compressed_set",
+             "compressed_to_dict", "compressed_from_dict", "save_compressed_json"}
+
+
+def __getattr__(name):
+    import importlib
+
+    if name in _IO_NAMES:
+        return getattr(importlib.import_module(".io", __package__), name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")

@@ -201,9 +201,48 @@ def io_cases(ss):
     print("io/: SPGR grid, kernel JSON, SPCK records + JSON mirrors")
 
 
+STATS_CASES = [
+    # (name, shape, d, r, A, B, steps, ExecConfig kwargs)
+    ("box2d_r1_64", "box", 2, 1, 64, 64, 1, {}),
+    ("box2d_r3_64_t2", "box", 2, 3, 64, 64, 2, {}),
+    ("star2d_r1_32_t2", "star", 2, 1, 32, 32, 2, {}),
+    ("box2d_r2_48_odd_unpacked", "box", 2, 2, 48, 48, 1, {"parity": "odd", "packing": False}),
+    ("box2d_r1_64_blocks32", "box", 2, 1, 64, 64, 1, {"a_block": 32, "b_block": 32}),
+    ("box2d_r1_30_noauto", "box", 2, 1, 30, 64, 1, {}),
+    ("box1d_r2_48_t3", "box", 1, 2, 1, 48, 3, {}),
+    ("box2d_r7_32", "box", 2, 7, 32, 32, 1, {}),
+]
+
+
+def stats_cases(ss):
+    """ExecStats.as_dict() of the reference execute on small grids (the
+    counter KATs: reference pipeline.py:200-259, tests/test_pipeline.py:140-192)."""
+    import json
+
+    out = {}
+    for name, shape, d, r, A, B, steps, kw in STATS_CASES:
+        span = 2 * r + 1
+        rng = np.random.default_rng([7, d, r, A, B])
+        coeffs = rng.uniform(0.5, 1.5, (span,) * d)
+        if shape == "star":
+            idx = np.indices((span,) * d)
+            on_axis = np.zeros((span,) * d, dtype=bool)
+            for ax in range(d):
+                on_axis |= np.all([idx[o] == r for o in range(d) if o != ax], axis=0) if d > 1 else True
+            coeffs = np.where(on_axis, coeffs, 0.0)
+        k = ss.make_kernel(shape, d, r, coeffs)
+        g = ss.random_grid(A, B, r, seed=[3, A, B])
+        cfg = ss.ExecConfig(**{k2: (ss.Parity(v) if k2 == "parity" else v) for k2, v in kw.items()})
+        _, st = ss.execute(k, g, steps, cfg)
+        out[name] = {"shape": shape, "d": d, "r": r, "A": A, "B": B, "steps": steps, "cfg": kw,
+                     "coeffs": np.asarray(coeffs).tolist(), "stats": st.as_dict()}
+    (OUT / "stats_golden.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+    print(f"stats_golden.json: {len(out)} cases")
+
+
 if __name__ == "__main__":
     ss = _ref()
-    transform_cases(ss)
-    naive_cases(ss)
-    naive3d_cases(ss)
-    io_cases(ss)
+    only = sys.argv[1:]
+    for fn in (transform_cases, naive_cases, naive3d_cases, io_cases, stats_cases):
+        if not only or fn.__name__ in only:
+            fn(ss)

@@ -483,8 +483,8 @@ def test_many_tiles_bf16_and_odd_parity(d, r, shape, dtype, parity):
 
 
 @pytest.mark.parametrize("shape", [(16, 16, 512), (40, 48, 256), (64, 64, 600)])
-def test_cta_pair_3d_bit_identical(monkeypatch, shape):
-    """3D CTA-pair mode (SPD_3D_CG2=1: one M = 256 tcgen05.mma.sp.cta_group::2
+def test_cta_pair_3d_bit_identical(shape):
+    """3D CTA-pair mode (SPD_PLAN_CTA_PAIR: one M = 256 tcgen05.mma.sp.cta_group::2
     per K-block, each CTA staging one x-half of B and holding one M-tile's
     A/E) gives the same bits as the default two-M-tile kernel."""
     from paper_2506_22035_b200.engine import Plan
@@ -496,9 +496,8 @@ def test_cta_pair_3d_bit_identical(monkeypatch, shape):
     torch.manual_seed(0)
     dense = torch.rand(tuple(n + 2 for n in shape), dtype=torch.float64, device="cuda") - 0.5
     outs = []
-    for cg2 in ("0", "1"):
-        monkeypatch.setenv("SPD_3D_CG2", cg2)
-        plan = Plan(k, sp.Parity.EVEN, "fp16")
+    for cg2 in (0, 1):
+        plan = Plan(k, sp.Parity.EVEN, "fp16", cta_pair=bool(cg2))
         assert plan.info().cg2 == int(cg2)
         g = DeviceGrid(plan, shape, 1)
         g.load_dense_f64(dense)
@@ -534,3 +533,41 @@ def test_concurrent_execute_callers(d, r, dims):
         t.join()
     for w, g in zip(want, got):
         np.testing.assert_array_equal(g, w)
+
+
+@pytest.mark.parametrize("d,r,dims", [(2, 1, (64, 512)), (2, 3, (48, 256)), (3, 1, (16, 16, 256))])
+def test_grid_cache_reuse_with_new_halo(d, r, dims):
+    """execute() reuses cached device grids between calls: a second call with a
+    different grid (different Dirichlet halo too) must give the same bits as a
+    call on freshly allocated buffers, and both match the oracle."""
+    from paper_2506_22035_b200.pipeline import release_device_grids
+
+    c = np.random.default_rng([d, r, 5]).uniform(0.5, 1.5, (2 * r + 1,) * d)
+    c /= c.sum()
+    k = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
+    cls = sp.Grid3D if d == 3 else sp.Grid
+    shape = tuple(n + 2 * r for n in dims)
+    g1 = cls(quant(np.random.default_rng(1).uniform(-1, 1, shape)).astype(np.float16), r)
+    g2 = cls(quant(np.random.default_rng(2).uniform(-1, 1, shape)).astype(np.float16), r)
+    release_device_grids()
+    sp.execute(k, g1, 3)
+    reused = sp.execute(k, g2, 3)[0].data.copy()
+    release_device_grids()
+    fresh = sp.execute(k, g2, 3)[0].data.copy()
+    np.testing.assert_array_equal(reused, fresh)
+    want = cnaive.naive_apply(k.coeffs, d, r, g2.data.astype(np.float64), r, 3)
+    assert max_rel_error(reused.astype(np.float64), want) < TOL["fp16"]
+
+
+def test_device_stats_equal_host_counters():
+    """The counters execute() returns are exec_stats()' plus the device block."""
+    from paper_2506_22035_b200.pipeline import exec_stats
+
+    k = rand_kernel("box", 2, 3, seed=4)
+    g = sp.random_grid(64, 64, 3, seed=20)
+    _, st = sp.execute(k, g, 2)
+    host = exec_stats(k, g, 2).as_dict()
+    dev = st.as_dict()
+    assert dev.pop("device")["mma_instructions"] > 0
+    host.pop("device")
+    assert dev == host
