@@ -165,6 +165,18 @@ int spd_run(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
  * launch ordered by per-band completion counters instead of one launch per
  * step (same results bit for bit). */
 #define SPD_RUN_PERSISTENT 1
+/* SPD_RUN_CHAINED: one launch per step, but every launch after the first
+ * skips the whole-grid dependency on its predecessor: each tile waits only for
+ * the previous step's three neighbouring tile bands (per-band completion
+ * counters published at gpu scope), so consecutive steps overlap at the
+ * launch boundary.  SPD_RUN_FORWARD: traverse every step's tiles in the same
+ * direction (default: alternate, for L2 reuse).  Same results bit for bit. */
+#define SPD_RUN_CHAINED 2
+#define SPD_RUN_FORWARD 4
+/* with SPD_RUN_PERSISTENT: plain step-major work order (every step's tiles
+ * forward, round-robin over the resident CTAs, no L2 sweeps); a tile still
+ * waits for the previous step's three neighbouring bands. */
+#define SPD_RUN_STEPMAJOR 8
 int spd_run_ex(const spd_plan* plan, const spd_grid_desc* g, void* buf0,
                void* buf1, int steps, int flags, void* stream);
 

@@ -98,6 +98,13 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Wait for a phase with the warp descheduled between tests: for the roles
+// that are off the critical path (publisher, poller), so their waiting does
+// not compete for issue slots and the mbarrier unit with the pipeline roles.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(128);
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -287,9 +294,18 @@ struct StepParams {
   // few wavefronts earlier, still resident in L2 (temporal blocking through
   // the 126 MB L2).
   int sweep, lag, total;     // total = pairs * per_band work items
+  int stepmajor;             // persistent (steps > 1) in plain step-major order: work item gi is tile
+                             // gi % n_tiles of step gi / n_tiles (no order array); every step
+                             // traverses its tiles forward
   int use_order;             // steps == 1 with a host-given band order (slab step: edge bands first)
   int publish;               // steps == 1: publish finished tiles to band_done (system scope) for a
                              // copy engine waiting on them (peer exchange inside one launch)
+  int chain;                 // chained one-step launches of a run (SPD_RUN_CHAINED): every tile is
+                             // published to band_done (gpu scope); launches after the run's first
+                             // one (chain_t >= 1) skip griddepcontrol.wait and instead wait per tile
+                             // for the three neighbouring bands of step chain_t - 1, so a step's
+                             // first tiles overlap the previous step's last ones
+  int chain_t;               // step index of this launch within the chained run
   const int2* order;         // [pairs] (step, band) in execution order (host-built)
   int64_t pitch, plane, origin;
   int64_t nx;                // x extent (interior)
@@ -315,6 +331,17 @@ struct StepParams {
 #endif
 #ifndef SPD_3D_NACC
 #define SPD_3D_NACC 4
+#endif
+// 2D r = 1: one B-image stage and four natural-row (TMA) stages.  The step
+// is bound by the memory system (tools/tma_bw.cu: the same TMA loads + 256-bit
+// stores with no compute take 82 us with two load stages, 68-70 us with four);
+// two B stages + two load stages measured B9 80.7 / W 210.0 us, one + four
+// 79.4 / 194.2 us (profiles/r02_stages.txt).
+#ifndef SPD_2D_NSTAGE
+#define SPD_2D_NSTAGE 1
+#endif
+#ifndef SPD_2D_NNAT
+#define SPD_2D_NNAT 4
 #endif
 #ifndef SPD_EPI_GROUPS
 #define SPD_EPI_GROUPS 1
@@ -574,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // allocation, resident A/E operands) overlaps the previous step kernel's
   // tail; the grids it reads and writes are touched only after the previous
   // grid has completed and its writes are visible.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.chain_t == 0 || SPD_DBG_BIT(1024)) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (threadIdx.x == 0) SPD_TRACE(14, 0);
   // Work order.  One step (steps == 1): tile t of the step, traversal
@@ -587,17 +614,20 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // the smallest unfinished tile can always proceed.  Static round-robin
   // over CTAs.
   const bool ordered = p.steps > 1 || p.use_order;
-  const bool publishing = p.steps > 1 || p.publish;
+  const bool publishing = p.steps > 1 || p.publish || p.chain;
+  // tiles wait (poller -> loader) for their inputs of the previous step
+  const bool dep_wait = p.steps > 1 || p.chain_t > 0;
   const int total = ordered ? p.total : p.n_tiles;
   struct TileId {
     int step, band;
+    int dep_step;  // step whose bands this tile's inputs come from + 1 (0: no wait)
     int64_t z0, y0, x0;
   };
   // Persistent order entries are fetched one tile ahead (the fetch for the
   // next tile is issued before this tile's work), so the dependent global
   // load never sits on a role's critical path.
   auto fetch = [&](int gi) -> int2 {
-    if (!ordered || gi >= total) return make_int2(0, 0);
+    if (!ordered || p.stepmajor || gi >= total) return make_int2(0, 0);
     return __ldg(p.order + gi / p.per_band);
   };
   auto decode_e = [&](int gi, int2 e) {
@@ -605,9 +635,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     int t;
     if (!ordered) {
       id.step = 0;
+      id.dep_step = p.chain_t;
       t = p.reverse ? p.n_tiles - 1 - gi : gi;
+    } else if (p.stepmajor) {
+      id.step = gi / p.n_tiles;
+      id.dep_step = id.step;
+      t = gi - id.step * p.n_tiles;
     } else {
       id.step = e.x;
+      id.dep_step = e.x;
       t = e.y * p.per_band + gi % p.per_band;
     }
     const int bx = t % p.tiles_x;
@@ -631,15 +667,15 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
   // with short tiles.
   // single-step publishing (slab step): only the two edge bands' tiles
   auto pub_tile = [&](const TileId& id) {
-    return p.steps > 1 || id.band == 0 || id.band == p.n_bands - 1;
+    return p.steps > 1 || p.chain || id.band == 0 || id.band == p.n_bands - 1;
   };
   auto publisher = [&]() {
-    if (p.steps == 1) {
+    if (p.steps == 1 && !p.chain) {
       int pit = 0;
       for (int gi = wid0; gi < total; gi += wstride) {
         const TileId id = decode_e(gi, fetch(gi));
         if (!pub_tile(id)) continue;
-        mbar_wait(bar_pubf + 8 * (pit % kNPub), (pit / kNPub) & 1);
+        mbar_wait_sleep(bar_pubf + 8 * (pit % kNPub), (pit / kNPub) & 1);
         asm volatile("fence.acq_rel.sys;" ::: "memory");  // observed by a copy engine
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
         mbar_arrive(bar_pube + 8 * (pit % kNPub));
@@ -649,12 +685,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
     int it = 0;
     for (int gi = wid0; gi < total;) {
-      mbar_wait(bar_pubf + 8 * (it % kNPub), (it / kNPub) & 1);
+      mbar_wait_sleep(bar_pubf + 8 * (it % kNPub), (it / kNPub) & 1);
       int n = 1;
       while (n < kNPub && gi + n * wstride < total &&
              mbar_test(bar_pubf + 8 * ((it + n) % kNPub), ((it + n) / kNPub) & 1))
         ++n;
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      if (!SPD_DBG_BIT(64)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
       for (int j = 0; j < n; ++j, ++it, gi += wstride) {
         const TileId id = decode_e(gi, fetch(gi));
         asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
@@ -683,12 +719,12 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         const uint32_t fb = bar_natf + 8 * ns;
         SPD_TRACE(0, it);
         mbar_wait(bar_nate + 8 * ns, nphase ^ 1);
-        if (p.steps > 1) {
+        if (dep_wait && !SPD_DBG_BIT(4096)) {
           // RAW/WAR across steps: the poller has seen the previous step's
           // neighbouring bands complete (gpu-scope acquire) and released this
           // slot; the CTA-scope acquire here extends that to the TMA reads.
           mbar_wait(bar_depf + 8 * (it % kDQ), (it / kDQ) & 1);
-          asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
+          if (!SPD_DBG_BIT(32)) asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> async-proxy reads
         }
         if (p.use_tmap) {
           // select between the two param-space descriptors (a runtime index
@@ -716,7 +752,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
             bulk_g2s(dst + b * C::ROW_BYTES, src, C::ROW_BYTES, fb);
           }
         }
-        if (p.steps > 1) mbar_arrive(bar_depe + 8 * (it % kDQ));
+        if (dep_wait && !SPD_DBG_BIT(4096)) mbar_arrive(bar_depe + 8 * (it % kDQ));
         SPD_TRACE(1, it);
       }
     }
@@ -927,20 +963,82 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
     }
     }
   } else if (warp == kPubWarp) {
-    if (publishing && lane == 0) publisher();
+    if (publishing && lane == 0 && !SPD_DBG_BIT(2048)) publisher();
   } else if (warp == kPollWarp) {
     // ===================== dependency poller (persistent launches) =========
     // Tiles whose dependencies are already met are released in batches of
     // up to kDQ/2 behind ONE acquire fence (a gpu-scope fence per tile cannot
     // keep up with 3D tiles).  A tile that must wait first flushes the batch:
     // its dependencies may be tiles of this very batch.
-    if (p.steps > 1 && lane == 0) {
+    if (dep_wait && lane == 0 && p.stepmajor && !SPD_DBG_BIT(4096)) {
+      // step-major order: a tile's dependencies lie about one step back and
+      // are nearly always met, so the poller's cost is its latency.  Tiles
+      // go in batches of kBatch: the loads of all their band counters are
+      // issued together (one L2 round trip per batch), then one acquire
+      // fence, then the batch is released to the loader.
+      constexpr int kBatch = kDQ / 2;
+      int it = 0;
+      for (int gi = wid0; gi < total;) {
+        int n = 0;
+        int need[kBatch], b0[kBatch], b1[kBatch], bb[kBatch];
+        bool any_dep = false;
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+          need[k] = 0;
+          b0[k] = b1[k] = bb[k] = 0;
+          const int g = gi + k * wstride;
+          if (g < total) {
+            const TileId id = decode_e(g, fetch(g));
+            mbar_wait_sleep(bar_depe + 8 * ((it + k) % kDQ), (((it + k) / kDQ) & 1) ^ 1);
+            if (id.dep_step > 0) {
+              need[k] = id.dep_step * p.per_band;
+              bb[k] = id.band;
+              b0[k] = id.band > 0 ? id.band - 1 : 0;
+              b1[k] = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
+              any_dep = true;
+            }
+            n = k + 1;
+          }
+        }
+        auto met = [&](int k) {
+          if (need[k] == 0 || SPD_DBG_BIT(128)) return true;
+          const unsigned int c0 = ld_relaxed_gpu(p.band_done + b0[k]);
+          const unsigned int c1 = ld_relaxed_gpu(p.band_done + bb[k]);
+          const unsigned int c2 = ld_relaxed_gpu(p.band_done + b1[k]);
+          return min(c0, min(c1, c2)) >= (unsigned int)need[k];
+        };
+        bool batch_ok = true;
+        if (any_dep) {
+          // one attempt for the whole batch (the loads go out together)
+          bool ok[kBatch];
+#pragma unroll
+          for (int k = 0; k < kBatch; ++k) ok[k] = k >= n || met(k);
+#pragma unroll
+          for (int k = 0; k < kBatch; ++k) batch_ok = batch_ok && ok[k];
+        }
+        if (batch_ok) {
+          if (any_dep && !SPD_DBG_BIT(512)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          for (int k = 0; k < n; ++k) mbar_arrive(bar_depf + 8 * ((it + k) % kDQ));
+        } else {
+          // slow path, tile by tile: a tile's dependencies may be earlier
+          // tiles of this very batch (small grids), which must be released
+          // before it is waited for
+          for (int k = 0; k < n; ++k) {
+            while (!met(k)) __nanosleep(64);
+            if (need[k] && !SPD_DBG_BIT(512)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            mbar_arrive(bar_depf + 8 * ((it + k) % kDQ));
+          }
+        }
+        it += n;
+        gi += n * wstride;
+      }
+    } else if (dep_wait && lane == 0 && !SPD_DBG_BIT(4096)) {
       constexpr int kBatch = kDQ / 2;
       int pending = 0;        // gathered, not yet released (tiles it-pending .. it-1)
       bool pend_dep = false;  // some pending tile has dependencies (needs the fence)
       auto flush = [&](int it_end) {
         if (pending == 0) return;
-        if (pend_dep) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        if (pend_dep && !SPD_DBG_BIT(512)) asm volatile("fence.acq_rel.gpu;" ::: "memory");
         for (int t = it_end - pending; t < it_end; ++t) mbar_arrive(bar_depf + 8 * (t % kDQ));
         pending = 0;
         pend_dep = false;
@@ -948,16 +1046,16 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
       int it = 0;
       for (int gi = wid0; gi < total; gi += wstride, ++it) {
         const TileId id = decode_e(gi, fetch(gi));
-        mbar_wait(bar_depe + 8 * (it % kDQ), ((it / kDQ) & 1) ^ 1);
-        if (id.step > 0) {
+        mbar_wait_sleep(bar_depe + 8 * (it % kDQ), ((it / kDQ) & 1) ^ 1);
+        if (id.dep_step > 0) {
           // a tile of step t reads the three neighbouring bands of step t-1
           // (RAW) and overwrites what step t-1 read (WAR): relaxed polls of
           // the three band counters
-          const unsigned int need = (unsigned int)(id.step * p.per_band);
+          const unsigned int need = (unsigned int)(id.dep_step * p.per_band);
           const int b0 = id.band > 0 ? id.band - 1 : 0;
           const int b1 = id.band + 1 < p.n_bands ? id.band + 1 : p.n_bands - 1;
           bool first = true;
-          while (true) {
+          while (!SPD_DBG_BIT(128)) {
             const unsigned int c0 = ld_relaxed_gpu(p.band_done + b0);
             const unsigned int c1 = ld_relaxed_gpu(p.band_done + id.band);
             const unsigned int c2 = ld_relaxed_gpu(p.band_done + b1);
@@ -1121,7 +1219,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
           }
           if (cb + 1 < NB) tmem_wait_ld();
         }
-        if (publishing && pub_tile(id)) {
+        if (publishing && pub_tile(id) && !SPD_DBG_BIT(2048)) {
           // hand the tile to the publisher warp (release at CTA scope after
           // the warp's stores); the gpu-scope release happens off this path
           const int ps = pit % kNPub;
@@ -1174,6 +1272,7 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         chunk_lim[mt] = (p.nx - xr) / L;
         orow[mt] = out + p.origin + z * p.plane + y * p.pitch + xr;
       }
+      if (warp == 0 && lane == 0) SPD_TRACE(12, it);
       mbar_wait(bar_accf + 8 * acc, aphase);
       tc_fence_after();
       if (warp == 0 && lane == 0) SPD_TRACE(8, it);
@@ -1287,11 +1386,10 @@ __global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_c
         if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(11, it);
         store(cb0, b0);
         store(cb1, b1);
-        if (warp == 0 && lane == 0 && pr == 0) SPD_TRACE(12, it);
         if (cb1 + 1 < TB) tmem_wait_ld();
       }
       if (warp == 0 && lane == 0) SPD_TRACE(9, it);
-      if (publishing && pub_tile(id)) {
+      if (publishing && pub_tile(id) && !SPD_DBG_BIT(2048)) {
         // hand the tile to the publisher warp (release at CTA scope after
         // the warp's stores); the gpu-scope release happens off this path
         const int ps = pit % kNPub;
@@ -1584,7 +1682,8 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   // <T, L, PARITY, NTILE, B-image stages, natural-row stages, accumulator
   //  stages, items per producer warp>; stage counts fill the 227 KB of smem
   // (scan in profiles/r01_tuning.txt).
-  if (g.L == 4 && g.n_tile == 128 && g.r_in == 34) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 34>(plan, sp, st);
+  if (g.L == 4 && g.n_tile == 128 && g.r_in == 34)
+    return launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, 3, 34>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
     return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40>(plan, sp, st);
@@ -2070,13 +2169,36 @@ int spd_run_ex(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* 
   // wavefront order (temporal blocking through L2), ordered by per-band
   // completion counters; bit-identical to the per-step launches.
   const bool persistent = (flags & SPD_RUN_PERSISTENT) != 0;
+  // SPD_RUN_CHAINED: one launch per step, but launches 1.. of the run wait per
+  // tile for the previous step's neighbouring bands (published counters)
+  // instead of for the whole previous grid
+  const bool chained = !persistent && (flags & SPD_RUN_CHAINED) != 0 && steps > 1 && plan->d >= 2 && !plan->g.cg2;
+  const bool forward = (flags & SPD_RUN_FORWARD) != 0;
   const int64_t extent = plan->d == 3 ? gd->nz : (plan->d == 2 ? gd->ny : 1);
+  unsigned int* chain_counters = nullptr;
   int done = 0;
   while (done < steps) {
     int chunk = persistent ? steps - done : 1;
     StepParams sp;
     rc = fill_step_params(plan, gd, done % 2 ? buf1 : buf0, done % 2 ? buf0 : buf1, 0, extent, chunk, sp);
     if (rc) return rc;
+    if (chained) {
+      if (!chain_counters) {
+        rc = launch_counters(sp.n_bands, (cudaStream_t)stream, &chain_counters);
+        if (rc) return rc;
+      }
+      sp.chain = 1;
+      sp.chain_t = done;
+      sp.band_done = chain_counters;
+      sp.reverse = forward ? 0 : (done & 1);
+      rc = dispatch(plan, sp, (cudaStream_t)stream);
+      if (rc) {
+        cudaFreeAsync(chain_counters, (cudaStream_t)stream);
+        return rc;
+      }
+      done += 1;
+      continue;
+    }
     if (chunk > 1) {
       // keep the work count in int range
       const int64_t cap = ((int64_t)1 << 30) / ((int64_t)sp.n_bands * sp.per_band);
@@ -2084,17 +2206,23 @@ int spd_run_ex(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* 
         chunk = (int)cap;
         sp.steps = chunk;
       }
-      rc = wavefront_order(plan, gd, sp);
-      if (rc) return rc;
+      if (flags & SPD_RUN_STEPMAJOR) {
+        sp.stepmajor = 1;
+        sp.total = sp.steps * sp.n_tiles;
+      } else {
+        rc = wavefront_order(plan, gd, sp);
+        if (rc) return rc;
+      }
       rc = launch_counters(sp.n_bands, (cudaStream_t)stream, &sp.band_done);
       if (rc) return rc;
     }
-    sp.reverse = persistent ? 0 : (done & 1);
+    sp.reverse = (persistent || forward) ? 0 : (done & 1);
     rc = dispatch(plan, sp, (cudaStream_t)stream);
     if (sp.band_done) cudaFreeAsync(sp.band_done, (cudaStream_t)stream);
     if (rc) return rc;
     done += chunk;
   }
+  if (chain_counters) cudaFreeAsync(chain_counters, (cudaStream_t)stream);
   return SPD_OK;
 }
 

@@ -22,6 +22,9 @@ from .transform import Parity
 
 TORCH_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
 SPD_PLAN_CTA_PAIR = 1  # include/spider.h
+SPD_RUN_PERSISTENT, SPD_RUN_CHAINED, SPD_RUN_FORWARD, SPD_RUN_STEPMAJOR = 1, 2, 4, 8  # include/spider.h
+# default spd_run_ex flags of DeviceGrid.run (one launch per step)
+RUN_FLAGS = 0
 NP_DTYPES = {"fp16": np.float16}
 
 
@@ -246,14 +249,17 @@ class DeviceGrid:
                                    C.c_void_p(host.data_ptr()), self._sp(stream)))
 
     @_on_device
-    def run(self, steps: int, stream=None, persistent: bool = False) -> None:
+    def run(self, steps: int, stream=None, persistent: bool = False, flags: int | None = None) -> None:
         """`steps` Jacobi steps on the device, ping-ponging the buffers
-        (one launch per step, or one persistent launch)."""
+        (one launch per step, or one persistent launch).  `flags` overrides
+        the spd_run_ex flags (SPD_RUN_*); default RUN_FLAGS."""
         if steps < 1:
             raise ValueError(f"step count must be >= 1, got {steps}")
+        if flags is None:
+            flags = SPD_RUN_PERSISTENT if persistent else RUN_FLAGS
         a, b = self.bufs[self.cur], self.bufs[1 - self.cur]
         check(lib.spd_run_ex(self.plan.handle, C.byref(self.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                             int(steps), 1 if persistent else 0, self._sp(stream)))
+                             int(steps), int(flags), self._sp(stream)))
         self.cur = (self.cur + steps) % 2
         self.step += steps
 

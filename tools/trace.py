@@ -13,7 +13,8 @@ desc, shape, d, r, kind, T = bench.CONFIGS[name]
 plan = get_plan(bench.make_kernel(kind, d, r), sp.Parity.EVEN, "fp16")
 g = DeviceGrid(plan, shape, r)
 g.load_dense_f64(torch.rand(g.dense_shape, dtype=torch.float64, device="cuda") - 0.5)
-g.run(4); torch.cuda.synchronize()
+flags = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+g.run(4, flags=flags); torch.cuda.synchronize()
 buf = (C.c_ulonglong * (8 * 16 * 64))()
 assert _lib.lib.spd_debug_trace(buf) == 0
 a = np.array(buf, dtype=np.int64).reshape(8, 16, 64)[0]
@@ -33,6 +34,8 @@ for e, nm in ((1, 'ld_issued'), (2, 'natfull'), (5, 'prod_done'), (7, 'mma'), (9
 lat = np.mean([(a[2, i] - a[1, i]) for i in range(3, n)]) / 1965
 prod = np.mean([(a[5, i] - a[3, i]) for i in range(3, n)]) / 1965
 epi = np.mean([(a[9, i] - a[8, i]) for i in range(3, n)]) / 1965
-sub = [np.mean([(a[e1, i] - a[e0, i]) for i in range(3, n)]) / 1965 for e0, e1 in ((8, 10), (10, 11), (11, 12))]
-print(f"epilogue batch 0: tmem load {sub[0]:.3f} us, pack+transpose {sub[1]:.3f} us, stores {sub[2]:.3f} us")
+sub = [np.mean([(a[e1, i] - a[e0, i]) for i in range(3, n)]) / 1965 for e0, e1 in ((8, 10), (10, 11))]
+gap = [np.mean([(a[e1, i + 1] - a[e0, i]) for i in range(3, n - 1)]) / 1965 for e0, e1 in ((9, 12), (12, 8))]
+print(f"epilogue batch 0: tmem load {sub[0]:.3f} us, pack+transpose {sub[1]:.3f} us; between tiles: "
+      f"loop {gap[0]:.3f} us, accumulator wait {gap[1]:.3f} us")
 print(f"TMA issue->natfull {lat:.3f} us  producer (bempty->last warp done) {prod:.3f} us  epilogue {epi:.3f} us")
