@@ -433,12 +433,22 @@ def run_ours(args, cfg_name):
             side[name]["config"] = workload_config(name, world)
 
     # end to end through the public API: pinned host fp16 grid in, result out.
+    # At N > 1 the whole job's grid (N slabs of the per-GPU grid) goes through
+    # one execute(..., DeviceConfig(devices=...)) call on rank 0, after the
+    # other ranks have left (they hold no GPU work while it runs).
     e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e and not args.force_slab:
+    if world > 1:
+        ctx.barrier()
+        ctx.dist.destroy_process_group()
+        if rank != 0:
+            return 0
+    if rank == 0 and not args.no_e2e and not args.force_slab:
         points_local = int(np.prod(shape))
-        dense_shape = tuple(s + 2 * r for s in shape)
-        e2e = e2e_rate(sp, make_kernel(kind, d, r), d, r, dense_shape, T, points_local, args.e2e_callers,
-                       max(2, min(args.steps, 4)))
+        glob = (shape[0] * world,) + tuple(shape[1:])
+        dense_shape = tuple(s + 2 * r for s in glob)
+        devices = None if world == 1 else tuple(k % torch.cuda.device_count() for k in range(world))
+        e2e = e2e_rate(sp, make_kernel(kind, d, r), d, r, dense_shape, T, points_local * world,
+                       args.e2e_callers if world == 1 else 1, max(2, min(args.steps, 4)), devices)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -471,19 +481,21 @@ def run_ours(args, cfg_name):
         if side:
             line["configs"] = side
         print(json.dumps(line), flush=True)
-    if world > 1:
-        ctx.dist.destroy_process_group()
     return 0
 
 
-def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
+def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller, devices=None):
     """End-to-end GStencil/s through `sp.execute` with host buffers.  Every
     call is a full execute() (H2D of its grid, T steps, D2H of the result);
     `callers` host threads issue calls concurrently, each on its own CUDA
     stream with its own pinned buffers, so one call's copies overlap another's
     steps (PCIe is full duplex) -- the way a server drives the engine.  Wall
-    clock over all calls; the one-caller figure is kept too."""
+    clock over all calls; the one-caller figure is kept too.  `devices`: the
+    multi-GPU form, execute(..., DeviceConfig(devices=devices)) (one caller).
+    """
     import torch
+
+    cfg = sp.DeviceConfig(devices=devices) if devices is not None else sp.DeviceConfig()
 
     cls = sp.Grid3D if d == 3 else sp.Grid
     bufs = []
@@ -503,10 +515,10 @@ def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
             try:
                 with torch.cuda.stream(streams[i]):
                     g_in, g_out = bufs[i]
-                    sp.execute(kern, g_in, T, out=g_out)  # warm (allocator, stream, grid cache)
+                    sp.execute(kern, g_in, T, cfg, out=g_out)  # warm (allocator, stream, grid cache)
                     start.wait()
                     for _ in range(n_calls):
-                        sp.execute(kern, g_in, T, out=g_out)
+                        sp.execute(kern, g_in, T, cfg, out=g_out)
             except BaseException as exc:  # surface worker failures
                 errors.append(exc)
                 start.abort()
@@ -534,7 +546,9 @@ def e2e_rate(sp, kern, d, r, dense_shape, T, points, callers, calls_per_caller):
             "d2h_bytes_per_step": nbytes, "ms_per_step": round(wc / nc * 1e3, 3),
             "callers": callers, "calls": nc, "timing": "host wall clock over all calls",
             "single_caller": {"value": round(single, 3), "ms_per_step": round(w1 / n1 * 1e3, 3)},
-            "api": "paper_2506_22035_b200.execute(kernel, Grid(pinned fp16), T, out=Grid(pinned fp16))"}
+            "api": ("paper_2506_22035_b200.execute(kernel, Grid(pinned fp16), T, "
+                    + (f"DeviceConfig(devices={tuple(devices)}), " if devices is not None else "")
+                    + "out=Grid(pinned fp16))")}
 
 
 # ---------------------------------------------------------------------------

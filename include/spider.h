@@ -283,6 +283,13 @@ int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, vo
                     spd_slab** out);
 int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream);
 int spd_slab_destroy(spd_slab* s);
+/* spd_slab_run: steps t0 .. t0+steps-1 of spd_slab_step in one call. */
+int spd_slab_run(spd_slab* s, int t0, int steps, void* compute_stream, void* comm_stream);
+/* spd_peer_enable: direct access from `device` to `peer` memory (one process
+ * driving several devices: execute(..., DeviceConfig(devices=...)) passes the
+ * neighbours' buffers straight to spd_slab_create).  No-op when equal;
+ * SPD_EUNSUPPORTED when the pair has no peer path. */
+int spd_peer_enable(int device, int peer);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ SIGNATURES = {
     "spd_slab_create": (_I, [_P, _DESC, _P, _P, _P, _P, _P, _DESC, _P, _P, _P, _DESC, _P, C.POINTER(_P)]),
     "spd_slab_step": (_I, [_P, _I, _P, _P]),
     "spd_slab_destroy": (_I, [_P]),
+    "spd_slab_run": (_I, [_P, _I, _I, _P, _P]),
+    "spd_peer_enable": (_I, [_I, _I]),
 }
 
 

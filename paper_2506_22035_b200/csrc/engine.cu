@@ -1787,9 +1787,25 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
 
 // buf0 holds the input of the launch's first step; steps > 1 alternate buffers
 // inside the (persistent) launch.
+// A host thread that has made no runtime call yet has no current context, and
+// the driver-API calls below (cuTensorMapEncodeTiled) then fail with
+// CUDA_ERROR_INVALID_CONTEXT: bind the current device's primary context once
+// per thread and device (cudaSetDevice of the device that is already current).
+static void bind_context() {
+  static thread_local uint64_t bound = 0;
+  int cur = 0;
+  if (cudaGetDevice(&cur) != cudaSuccess) return;
+  const uint64_t bit = 1ull << (cur & 63);
+  if (!(bound & bit)) {
+    cudaSetDevice(cur);
+    bound |= bit;
+  }
+}
+
 static int fill_step_params(const spd_plan* plan, const spd_grid_desc* gd, const void* buf0, void* buf1, int64_t lo,
                             int64_t hi, int steps, StepParams& sp) {
   const Geometry& g = plan->g;
+  bind_context();
   std::memset(&sp, 0, sizeof(sp));
   sp.g = g;
   sp.buf[0] = const_cast<void*>(buf0);

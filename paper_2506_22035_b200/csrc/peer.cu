@@ -309,4 +309,38 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
   return SPD_OK;
 }
 
+// All steps of a run in one call (the host loop of one device; a process
+// driving several devices runs one such call per device on its own thread).
+int spd_slab_run(spd_slab* s, int t0, int steps, void* compute_stream, void* comm_stream) {
+  using namespace spd;
+  if (!s) return set_error(SPD_EINVAL, "null slab");
+  if (t0 < 0 || steps < 1) return set_error(SPD_EINVAL, "bad step range (t0 %d, steps %d)", t0, steps);
+  for (int t = t0; t < t0 + steps; ++t) {
+    int rc = spd_slab_step(s, t, compute_stream, comm_stream);
+    if (rc) return rc;
+  }
+  return SPD_OK;
+}
+
+// Direct peer access from `device` to `peer` (single-process multi-device
+// slabs: the neighbours' buffers and flag words are plain device pointers).
+int spd_peer_enable(int device, int peer) {
+  using namespace spd;
+  if (device == peer) return SPD_OK;
+  int can = 0;
+  int rc = rt_err(cudaDeviceCanAccessPeer(&can, device, peer), "cudaDeviceCanAccessPeer");
+  if (rc) return rc;
+  if (!can) return set_error(SPD_EUNSUPPORTED, "device %d cannot access peer device %d", device, peer);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the (non-sticky) error it recorded
+    e = cudaSuccess;
+  }
+  cudaSetDevice(prev);
+  return rt_err(e, "cudaDeviceEnablePeerAccess");
+}
+
 }  // extern "C"

@@ -20,8 +20,10 @@ against `SlabOps` so the exchange logic is tested with gloo on CPU
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -364,3 +366,160 @@ class PeerSlab:
 
 
 __all__ += ["PeerSlab"]
+
+
+# ---------------------------------------------------------------------------
+# Several devices driven by one process: execute(..., DeviceConfig(devices=...))
+
+
+def enable_peer_access(devices) -> None:
+    """Direct peer access between neighbouring devices of a slab chain (both
+    directions); raises ValueError when a pair has no peer path."""
+    for a, b in zip(devices, devices[1:]):
+        if a != b:
+            check(lib.spd_peer_enable(int(a), int(b)))
+            check(lib.spd_peer_enable(int(b), int(a)))
+
+
+class LocalSlabs:
+    """A grid cut into slabs along y (2D) / z (3D), one per entry of
+    `devices` (entries may repeat: several slabs on one device), all driven
+    by this process.  The halo exchange is the peer-memory one of PeerSlab
+    (csrc/peer.cu: boundary bands published by the step kernel, copy engine
+    into the neighbour's halo rows, stream-memory-op flags), with the
+    neighbours' buffers passed as plain device pointers instead of IPC
+    mappings.  Each slab's steps are issued by one native call
+    (spd_slab_run) on its own host thread, so the host cost does not grow
+    with the device count.
+
+    `plans` maps device -> Plan; `shape` is the global interior shape."""
+
+    def __init__(self, plans: dict, devices, shape, halo: int):
+        devices = [int(v) for v in devices]
+        if not devices:
+            raise ValueError("no devices given")
+        plan0 = plans[devices[0]]
+        d = plan0.kernel.d
+        if d == 1:
+            raise ValueError("1D grids cannot be cut into slabs")
+        info = plan0.info()
+        self.band = info.tile_z if d == 3 else info.tile_y
+        self.devices, self.shape, self.halo, self.d = devices, tuple(int(v) for v in shape), int(halo), d
+        world = len(devices)
+        self.slabs = [decompose(self.shape[0], world, k, align=self.band) for k in range(world)]
+        if any(s.rows < self.halo for s in self.slabs):
+            raise ValueError(f"{self.shape[0]} rows give slabs thinner than the halo ({self.halo})")
+        enable_peer_access(devices)
+        self.grids = []
+        self.flags = []
+        self.streams = []
+        for dev, slab in zip(devices, self.slabs):
+            with torch.cuda.device(dev):
+                self.grids.append(DeviceGrid(plans[dev], (slab.rows,) + self.shape[1:], self.halo))
+                self.flags.append(torch.zeros(2, dtype=torch.int32, device=torch.device("cuda", dev)))
+                self.streams.append((torch.cuda.Stream(dev), torch.cuda.Stream(dev)))
+        self.handles = []
+
+    def _create_handles(self) -> None:
+        """Exchange handles over the neighbours' buffers; only once every
+        slab holds its initial state (both buffers, halos included)."""
+        null = None
+        for k, (dev, g) in enumerate(zip(self.devices, self.grids)):
+            up = self.grids[k - 1] if k > 0 else None
+            dn = self.grids[k + 1] if k + 1 < len(self.grids) else None
+
+            def ptrs(n, j):
+                if n is None:
+                    return null, null, null, null
+                return (C.c_void_p(n.bufs[0].data_ptr()), C.c_void_p(n.bufs[1].data_ptr()), C.byref(n.desc),
+                        C.c_void_p(self.flags[j].data_ptr()))
+
+            h = C.c_void_p()
+            with torch.cuda.device(dev):
+                check(lib.spd_slab_create(g.plan.handle, C.byref(g.desc), C.c_void_p(g.bufs[0].data_ptr()),
+                                          C.c_void_p(g.bufs[1].data_ptr()), C.c_void_p(self.flags[k].data_ptr()),
+                                          *ptrs(up, k - 1), *ptrs(dn, k + 1), C.byref(h)))
+            self.handles.append(h)
+
+    def _each(self, fn) -> None:
+        """fn(k) on one host thread per slab, each with its device current;
+        the first failure is re-raised."""
+        errors = []
+
+        def body(k):
+            try:
+                with torch.cuda.device(self.devices[k]):
+                    fn(k)
+            except BaseException as exc:  # noqa: BLE001 - re-raised below
+                errors.append(exc)
+
+        threads = [threading.Thread(target=body, args=(k,)) for k in range(len(self.devices))]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+
+    def run(self, data, steps: int, native16: bool, out):
+        """`steps` steps of the dense host grid `data` (halo included);
+        returns the dense result (written into `out` when given)."""
+        h = self.halo
+        res = out if out is not None else np.empty(data.shape, dtype=np.float16 if native16 else np.float64)
+
+        def load(k):
+            s, g, (cs, _) = self.slabs[k], self.grids[k], self.streams[k]
+            part = np.ascontiguousarray(data[s.lo : s.hi + 2 * h])
+            if native16:
+                g.upload(torch.from_numpy(part), stream=cs)
+            else:
+                g.load_dense_f64(torch.from_numpy(part.astype(np.float64, copy=False)).to(g.device), stream=cs)
+            cs.synchronize()
+
+        self._each(load)  # every halo holds its initial neighbour rows before any exchange writes
+        self._create_handles()
+        try:
+            def steps_of(k):
+                cs, xs = self.streams[k]
+                check(lib.spd_slab_run(self.handles[k], 0, int(steps), C.c_void_p(cs.cuda_stream),
+                                       C.c_void_p(xs.cuda_stream)))
+                cs.synchronize()
+                xs.synchronize()
+
+            self._each(steps_of)
+        finally:
+            for dev, hd in zip(self.devices, self.handles):
+                with torch.cuda.device(dev):
+                    torch.cuda.synchronize(dev)
+                    lib.spd_slab_destroy(hd)
+            self.handles = []
+        for g in self.grids:
+            g.cur, g.step = steps % 2, g.step + steps
+
+        def store(k):
+            s, g, (cs, _) = self.slabs[k], self.grids[k], self.streams[k]
+            lo, hi = s.lo + h, s.hi + h  # dense rows of the slab interior
+            if k == 0:
+                lo = 0
+            if k == len(self.slabs) - 1:
+                hi = res.shape[0]
+            if native16:
+                tmp = torch.empty(g.dense_shape, dtype=torch.float16, pin_memory=True)
+                g.download(tmp, stream=cs)
+                cs.synchronize()
+                res[lo:hi] = tmp.numpy()[lo - s.lo : hi - s.lo]
+            else:
+                with torch.cuda.stream(cs):
+                    part = g.to_dense_f64(stream=cs).cpu().numpy()
+                res[lo:hi] = part[lo - s.lo : hi - s.lo].astype(res.dtype, copy=False)
+
+        self._each(store)
+        return res
+
+
+def execute_slabs(plans: dict, devices, shape, halo: int, data, steps: int, native16: bool, out=None):
+    """One-process multi-device run (see LocalSlabs)."""
+    return LocalSlabs(plans, devices, shape, halo).run(data, steps, native16, out)
+
+
+__all__ += ["LocalSlabs", "enable_peer_access", "execute_slabs"]

@@ -67,16 +67,30 @@ class ExecConfig:
 
 @dataclass(frozen=True)
 class DeviceConfig:
-    """Device-path knobs: storage dtype of the grid on the B200 and parity."""
+    """Device-path knobs: storage dtype of the grid on the B200 and parity.
+
+    `devices`: run on several GPUs from this process -- the grid is cut into
+    slabs along y (2D) / z (3D), one per listed device, with the halo rows
+    exchanged through peer memory every step (distributed.LocalSlabs).  A
+    device may be listed more than once (several slabs on one GPU).  Results
+    are bit-identical to the one-device run."""
 
     parity: Parity = Parity.EVEN
     dtype: str = "fp16"
     device: int | None = None
+    devices: tuple | None = None
 
     def __post_init__(self) -> None:
         if self.dtype not in TORCH_DTYPES:
             raise ValueError(f"device dtype must be one of {sorted(TORCH_DTYPES)}")
         object.__setattr__(self, "parity", Parity(self.parity))
+        if self.devices is not None:
+            devs = tuple(int(v) for v in self.devices)
+            if not devs or any(v < 0 for v in devs):
+                raise ValueError(f"bad device list {self.devices!r}")
+            if self.device is not None and self.device != devs[0]:
+                raise ValueError("give either device or devices")
+            object.__setattr__(self, "devices", devs)
 
 
 @dataclass
@@ -318,10 +332,15 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
     quantised on the device and the result is returned as float64 (float32
     inputs give float32).  The work runs on the plan's device (DeviceConfig
     .device, default the current one), on that device's current stream.
+    With `DeviceConfig(devices=(d0, d1, ...))` the grid is split into slabs
+    across those devices (one host thread per slab, peer-memory halo
+    exchange; distributed.LocalSlabs), same result bit for bit.
     """
     _check_inputs(kernel, grid, steps)
     dcfg = _device_cfg(cfg)
-    plan = get_plan(kernel, dcfg.parity, dcfg.dtype, dcfg.device)
+    devices = dcfg.devices if dcfg.devices is not None and len(dcfg.devices) > 1 else None
+    first = dcfg.devices[0] if dcfg.devices is not None else dcfg.device
+    plan = get_plan(kernel, dcfg.parity, dcfg.dtype, first)
     stats = _stats(kernel, grid, steps, cfg, plan)  # raises the reference's tile-plan errors first
     shape = (grid.Z, grid.A, grid.B) if kernel.d == 3 else (grid.A, grid.B)
     data = grid.data
@@ -329,6 +348,22 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
     if native16 and out is not None:
         if out.data.shape != data.shape or out.data.dtype != np.float16 or not out.data.flags.c_contiguous:
             raise ValueError("out grid must be a contiguous float16 array of the input's shape")
+    if devices is not None:
+        from .distributed import execute_slabs
+
+        plans = {dev: get_plan(kernel, dcfg.parity, dcfg.dtype, dev) for dev in set(devices)}
+        target = out.data if (native16 and out is not None) else None
+        res = execute_slabs(plans, devices, shape, grid.halo, data, steps, native16, target)
+        if not native16:
+            if data.dtype == np.float32:
+                res = res.astype(np.float32)
+            if out is not None:
+                out.data[...] = res
+                res = out.data
+        stats.device["devices"] = list(devices)
+        stats.device["exchange"] = "peer memory (spd_slab_run), one slab per listed device"
+        cls = Grid3D if kernel.d == 3 else Grid
+        return cls(res, grid.halo, grid.step + steps), stats
     with torch.cuda.device(plan.device):
         dg = _GRIDS.acquire(plan, shape, grid.halo)
         try:

@@ -20,7 +20,7 @@ def test_bench_two_ranks_self_launched():
     env = dict(os.environ, SPD_BENCH_BACKEND="gloo")
     env.pop("WORLD_SIZE", None)
     out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
-                          "--no-cpu-baseline", "--no-e2e"], capture_output=True, text=True, timeout=900,
+                          "--no-cpu-baseline"], capture_output=True, text=True, timeout=900,
                          cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -30,6 +30,9 @@ def test_bench_two_ranks_self_launched():
     assert line["impl_detail"]["exchange"] == "peer", out.stderr[-2000:]
     assert "W" in line["configs"] and line["configs"]["W"]["value"] > 0
     assert line["roofline"]["frac"] > 0 and line["gpu_launches"] > 0
+    # e2e at N = 2: the whole job's grid through execute(..., DeviceConfig(devices=(0, 0)))
+    assert line["e2e"]["value"] > 0 and "devices=(0, 0)" in line["e2e"]["api"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 2 * (2 * 10240 + 2) * (10240 + 2)
 
 
 @pytest.mark.gpu

@@ -1,0 +1,70 @@
+"""execute(..., DeviceConfig(devices=...)): one process, the grid cut into
+slabs over several devices with the peer-memory halo exchange.  The box has
+one GPU, so the slabs share cuda:0 (listed several times); the exchange runs
+the same code as between NVLink peers (plain device pointers, copy engine,
+stream memory operations).  Results must equal the one-device execute bit
+for bit."""
+import numpy as np
+import pytest
+
+import paper_2506_22035_b200 as sp
+from paper_2506_22035_b200.pipeline import DeviceConfig
+
+gpu = pytest.mark.gpu
+
+
+def _kernel(d, r, seed=3):
+    rng = np.random.default_rng([d, r, seed])
+    c = rng.uniform(0.5, 1.5, (2 * r + 1,) * d)
+    c /= c.sum()
+    return sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
+
+
+def _grid(d, r, shape, dtype):
+    rng = np.random.default_rng([len(shape), *shape])
+    data = rng.uniform(-1, 1, tuple(s + 2 * r for s in shape)).astype(dtype)
+    return sp.Grid3D(data, r) if d == 3 else sp.Grid(data, r)
+
+
+@gpu
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("d,r,shape,n,steps,dtype", [
+    (2, 1, (256, 1024), 2, 7, np.float16),
+    (2, 1, (224, 512), 3, 4, np.float16),      # ragged last slab
+    (2, 3, (96, 1024), 2, 3, np.float16),
+    (2, 1, (128, 512), 2, 5, np.float64),      # quantised on the device, fp64 result
+    (3, 1, (48, 24, 256), 3, 3, np.float16),
+    (3, 1, (32, 16, 128), 2, 2, np.float32),
+])
+def test_multidevice_execute_matches_one_device(d, r, shape, n, steps, dtype):
+    k = _kernel(d, r)
+    g = _grid(d, r, shape, dtype)
+    before = g.data.copy()
+    want, _ = sp.execute(k, g, steps, DeviceConfig())
+    got, stats = sp.execute(k, g, steps, DeviceConfig(devices=(0,) * n))
+    assert np.array_equal(g.data, before), "input grid modified"
+    assert got.data.dtype == want.data.dtype
+    assert got.step == want.step == steps
+    assert np.array_equal(got.data, want.data)
+    assert stats.device["devices"] == [0] * n
+
+
+@gpu
+@pytest.mark.timeout(300, method="thread")
+def test_multidevice_execute_into_out_grid_repeated():
+    k = _kernel(2, 1)
+    g = _grid(2, 1, (512, 1024), np.float16)
+    want, _ = sp.execute(k, g, 9)
+    out = sp.Grid(np.empty_like(g.data), 1)
+    for _ in range(2):  # fresh slabs and counters per call
+        got, _ = sp.execute(k, g, 9, DeviceConfig(devices=(0, 0)), out=out)
+        assert got.data is out.data
+        assert np.array_equal(out.data, want.data)
+
+
+@gpu
+def test_multidevice_rejects_too_many_slabs():
+    k = _kernel(2, 1)
+    g = _grid(2, 1, (64, 512), np.float16)  # two 32-row bands
+    with pytest.raises(ValueError):
+        sp.execute(k, g, 2, DeviceConfig(devices=(0, 0, 0)))
