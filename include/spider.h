@@ -218,6 +218,11 @@ int spd_upload(const spd_grid_desc* g, const void* host_dense, void* dev,
                void* stream);
 int spd_download(const spd_grid_desc* g, const void* dev, void* host_dense,
                  void* stream);
+/* Dense rows (2D) / planes (3D) [lo, hi) (dense coordinates: 0 is the first
+ * halo row) of the grid into the same rows of host_dense, the whole grid's
+ * dense host array; nothing else is written (streamed execute). */
+int spd_download_rows(const spd_grid_desc* g, const void* dev, void* host_dense,
+                      int64_t lo, int64_t hi, void* stream);
 
 /* Same transfers through a caller-owned device staging buffer of the dense
  * size ((nz+2h)(ny+2h)(nx+2h) 16-bit elements): one linear DMA plus a

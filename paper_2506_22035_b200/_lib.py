@@ -82,6 +82,7 @@ SIGNATURES = {
     "spd_unpack_grid": (_I, [_DESC, _I, _P, _P, _P]),
     "spd_upload": (_I, [_DESC, _P, _P, _P]),
     "spd_download": (_I, [_DESC, _P, _P, _P]),
+    "spd_download_rows": (_I, [_DESC, _P, _P, _I64, _I64, _P]),
     "spd_upload_staged": (_I, [_DESC, _P, _P, _P, _P]),
     "spd_download_staged": (_I, [_DESC, _P, _P, _P, _P]),
     "spd_copy_halo": (_I, [_DESC, _P, _P, _P]),

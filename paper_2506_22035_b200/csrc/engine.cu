@@ -349,24 +349,45 @@ struct StepParams {
 #ifndef SPD_PROD_WARPS
 #define SPD_PROD_WARPS 8
 #endif
+// Producer warps per geometry (tools/time_cfg.py over builds, profiles/r02_prodwarps.txt):
+// 2D r = 1 keeps 8; the 3D two-M-tile geometry runs fastest with 4 (B27
+// 140.0 -> 122.3 us; 2: 422, 3: 176, 5: 138), 2D r = 3 with 5 (B49 101.9 ->
+// 97.2 us; 4: 115, 6: 99.0, 7: 100.6).
+#ifndef SPD_3D_PW
+#define SPD_3D_PW 4
+#endif
+#ifndef SPD_L8_PW
+#define SPD_L8_PW 5
+#endif
+#ifndef SPD_GEN_PW
+#define SPD_GEN_PW 8
+#endif
 constexpr int kEpiGroups = SPD_EPI_GROUPS;
 constexpr int kEpiWarps = 4;                          // warps per epilogue group
 constexpr int kEpiAll = kEpiWarps * kEpiGroups;       // warps 0 .. kEpiAll-1
-constexpr int kProdWarps = SPD_PROD_WARPS;
-constexpr int kMmaWarp = kEpiAll + kProdWarps;
-constexpr int kLoadWarp = kMmaWarp + 1;
+// Producer warps: a per-geometry template parameter (PW below; this is its
+// default).  Warp roles of a CTA with PW producers: epilogue 0..kEpiAll-1,
+// producers kEpiAll..kEpiAll+PW-1, then MMA, loader, publisher, poller.
 // Persistent launches only (idle in one-step launches): the publisher makes
 // finished tiles visible and bumps band counters; the poller runs up to kDQ
 // tiles ahead of the loader, waiting for each tile's dependencies (so the
 // loader never holds an L2 round trip + gpu-scope fence on its path).
-constexpr int kPubWarp = kLoadWarp + 1;
-constexpr int kPollWarp = kPubWarp + 1;
-constexpr int kThreads = 32 * (kPollWarp + 1);
+constexpr int kProdWarpsDefault = SPD_PROD_WARPS;
+template <int PW>
+struct Roles {
+  static constexpr int kProdWarps = PW;
+  static constexpr int kMmaWarp = kEpiAll + PW;
+  static constexpr int kLoadWarp = kMmaWarp + 1;
+  static constexpr int kPubWarp = kLoadWarp + 1;
+  static constexpr int kPollWarp = kPubWarp + 1;
+  static constexpr int kThreads = 32 * (kPollWarp + 1);
+};
 constexpr int kDQ = 8;                   // poller -> loader ring depth
 constexpr int kNPub = 8;                 // publish ring depth (max tiles per publish batch)
 
-template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
-struct Cfg {
+template <int L, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false,
+          int PW = kProdWarpsDefault>
+struct Cfg : Roles<PW> {
   // fast paths: L = 4 (r = 1) and L = 8 (r = 3); any other even L up to 16 uses
   // the generic producer / epilogue
   static constexpr bool GEN = !(L == 4 || L == 8);
@@ -406,7 +427,7 @@ struct Cfg {
   // MMA schedule: the first M-tile's input rows; M-tile t uses them shifted
   // by t*MTR rows (same A/E images)
   static constexpr int RIN_MMA = RIN - (MT - 1) * MTR;
-  static constexpr int NQ = (N_ITEMS + kProdWarps - 1) / kProdWarps;
+  static constexpr int NQ = (N_ITEMS + PW - 1) / PW;
 };
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
@@ -493,9 +514,15 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
 //   loader --(nat_full: tx bytes)--> producers --(nat_empty)--> loader
 //   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
 //   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
-__global__ void __launch_bounds__(kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2>;
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0,
+          bool CG2 = false, int PW = kProdWarpsDefault>
+__global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
+  constexpr int kProdWarps = C::kProdWarps;
+  constexpr int kMmaWarp = C::kMmaWarp;
+  constexpr int kLoadWarp = C::kLoadWarp;
+  constexpr int kPubWarp = C::kPubWarp;
+  constexpr int kPollWarp = C::kPollWarp;
   constexpr int KC = C::KC;
   constexpr int NQ = C::NQ;
   const Geometry& g = p.g;
@@ -1609,11 +1636,12 @@ static int launch_counters(int n, cudaStream_t st, unsigned int** out) {
   return cuda_err(cudaMemsetAsync(*out, 0, sizeof(unsigned int) * n, st), "counter reset");
 }
 
-template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0, bool CG2 = false>
+template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0,
+          bool CG2 = false, int PW = kProdWarpsDefault>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
-  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2>;
+  using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
   if (CG2 != (plan->g.cg2 != 0)) return set_error(SPD_EUNSUPPORTED, "CTA-pair geometry mismatch");
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2>;
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
   {  // the MMA issuer's compile-time schedule must be the plan's
     constexpr int RPM = 4 / C::KC;
@@ -1651,7 +1679,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
   if (CG2 && sp.steps > 1) return set_error(SPD_EUNSUPPORTED, "persistent launch not supported in CTA-pair mode");
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
@@ -1686,22 +1714,24 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
     return launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, 3, 34>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
-    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40>(plan, sp, st);
+    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40, false, SPD_3D_PW>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.cg2)
-    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, 3, 100, 1, 0, true>(plan, sp, st);
-  if (g.L == 8 && g.n_tile == 64 && g.r_in == 22) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 22>(plan, sp, st);
-  if (g.L == 8 && g.n_tile == 64 && g.r_in == 16) return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16>(plan, sp, st);
+    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, 3, 100, 1, 0, true, SPD_3D_PW>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64 && g.r_in == 22)
+    return launch_step<T, 8, PARITY, 64, 3, 4, 4, 22, 1, 0, false, SPD_L8_PW>(plan, sp, st);
+  if (g.L == 8 && g.n_tile == 64 && g.r_in == 16)
+    return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16, 1, 0, false, SPD_L8_PW>(plan, sp, st);
   // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
-  if (g.L == 6 && g.r_in == 25) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 25>(plan, sp, st);
-  if (g.L == 6 && g.r_in == 21) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 21>(plan, sp, st);
-  if (g.L == 10 && g.r_in == 20) return launch_step<T, 10, PARITY, 64, 2, 1, 4, 20>(plan, sp, st);
-  if (g.L == 10 && g.r_in == 12) return launch_step<T, 10, PARITY, 64, 2, 2, 4, 12>(plan, sp, st);
-  if (g.L == 12 && g.r_in == 20) return launch_step<T, 12, PARITY, 64, 2, 1, 4, 20>(plan, sp, st);
-  if (g.L == 12 && g.r_in == 10) return launch_step<T, 12, PARITY, 64, 2, 2, 4, 10>(plan, sp, st);
-  if (g.L == 14 && g.r_in == 21) return launch_step<T, 14, PARITY, 64, 2, 1, 4, 21>(plan, sp, st);
-  if (g.L == 14 && g.r_in == 9) return launch_step<T, 14, PARITY, 64, 2, 2, 4, 9>(plan, sp, st);
-  if (g.L == 16 && g.r_in == 22) return launch_step<T, 16, PARITY, 64, 1, 1, 4, 22>(plan, sp, st);
-  if (g.L == 16 && g.r_in == 8) return launch_step<T, 16, PARITY, 64, 2, 2, 4, 8>(plan, sp, st);
+  if (g.L == 6 && g.r_in == 25) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 25, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 6 && g.r_in == 21) return launch_step<T, 6, PARITY, 64, 2, 3, 4, 21, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 10 && g.r_in == 20) return launch_step<T, 10, PARITY, 64, 2, 1, 4, 20, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 10 && g.r_in == 12) return launch_step<T, 10, PARITY, 64, 2, 2, 4, 12, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 12 && g.r_in == 20) return launch_step<T, 12, PARITY, 64, 2, 1, 4, 20, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 12 && g.r_in == 10) return launch_step<T, 12, PARITY, 64, 2, 2, 4, 10, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 14 && g.r_in == 21) return launch_step<T, 14, PARITY, 64, 2, 1, 4, 21, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 14 && g.r_in == 9) return launch_step<T, 14, PARITY, 64, 2, 2, 4, 9, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 16 && g.r_in == 22) return launch_step<T, 16, PARITY, 64, 1, 1, 4, 22, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
+  if (g.L == 16 && g.r_in == 8) return launch_step<T, 16, PARITY, 64, 2, 2, 4, 8, 1, 0, false, SPD_GEN_PW>(plan, sp, st);
   return set_error(SPD_EUNSUPPORTED, "no kernel instantiation for L=%d n_tile=%d", g.L, g.n_tile);
 }
 
@@ -2310,6 +2340,32 @@ int spd_download(const spd_grid_desc* g, const void* dev, void* host_dense, void
   if (!g || !host_dense || !dev) return spd::set_error(SPD_EINVAL, "null argument");
   cudaMemcpy3DParms p = copy_parms(g, const_cast<void*>(dev), host_dense, false);
   return spd::cuda_err(cudaMemcpy3DAsync(&p, (cudaStream_t)stream), "spd_download");
+}
+
+// Dense rows (2D) / planes (3D) [lo, hi) of the grid into the same rows of
+// the host dense array (the whole grid's array; only those rows are written):
+// a streamed execute downloads each window's finished slab this way.
+int spd_download_rows(const spd_grid_desc* g, const void* dev, void* host_dense, int64_t lo, int64_t hi,
+                      void* stream) {
+  if (!g || !host_dense || !dev) return spd::set_error(SPD_EINVAL, "null argument");
+  const int64_t h = g->halo;
+  const int64_t nxd = g->nx + 2 * h, nyd = g->ny + 2 * h;
+  const int64_t units = g->dims == 3 ? g->nz + 2 * h : nyd;
+  if (g->dims == 1) return spd::set_error(SPD_EINVAL, "row ranges are defined for 2D / 3D grids");
+  if (lo < 0 || hi > units || lo >= hi) return spd::set_error(SPD_EINVAL, "bad row range [%lld, %lld) of %lld",
+                                                              (long long)lo, (long long)hi, (long long)units);
+  cudaMemcpy3DParms p = copy_parms(g, const_cast<void*>(dev), host_dense, false);
+  if (g->dims == 3) {
+    p.srcPtr.ptr = (char*)p.srcPtr.ptr + 2 * lo * g->plane;
+    p.dstPtr.ptr = (char*)p.dstPtr.ptr + 2 * lo * nyd * nxd;
+    p.extent.depth = (size_t)(hi - lo);
+  } else {
+    p.srcPtr.ptr = (char*)p.srcPtr.ptr + 2 * lo * g->pitch;
+    p.dstPtr.ptr = (char*)p.dstPtr.ptr + 2 * lo * nxd;
+    p.extent.height = (size_t)(hi - lo);
+    p.dstPtr.ysize = (size_t)(hi - lo);
+  }
+  return spd::cuda_err(cudaMemcpy3DAsync(&p, (cudaStream_t)stream), "spd_download_rows");
 }
 
 // Staged transfers: one linear DMA between the host dense array and a

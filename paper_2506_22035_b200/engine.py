@@ -249,6 +249,14 @@ class DeviceGrid:
                                    C.c_void_p(host.data_ptr()), self._sp(stream)))
 
     @_on_device
+    def download_rows(self, host_ptr: int, lo: int, hi: int, stream=None) -> None:
+        """Dense rows (2D) / planes (3D) [lo, hi) of the current buffer into
+        the same rows of a host dense array starting at `host_ptr` (the
+        array's first halo row; only those rows are written)."""
+        check(lib.spd_download_rows(C.byref(self.desc), C.c_void_p(self.bufs[self.cur].data_ptr()),
+                                    C.c_void_p(int(host_ptr)), int(lo), int(hi), self._sp(stream)))
+
+    @_on_device
     def run(self, steps: int, stream=None, persistent: bool = False, flags: int | None = None) -> None:
         """`steps` Jacobi steps on the device, ping-ponging the buffers
         (one launch per step, or one persistent launch).  `flags` overrides

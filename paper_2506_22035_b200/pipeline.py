@@ -19,6 +19,7 @@ hot path moved to the B200:
 from __future__ import annotations
 
 import json
+import os
 import threading
 from dataclasses import dataclass, field, replace
 
@@ -286,7 +287,7 @@ class _GridPool:
     region is ever written, so the zero padding the kernels rely on survives
     reuse.  `release_device_grids()` frees the cache."""
 
-    def __init__(self, keep: int = 4):
+    def __init__(self, keep: int = 8):
         self.keep = keep
         self._free: dict = {}
         self._lock = threading.Lock()
@@ -318,6 +319,92 @@ _GRIDS = _GridPool()
 def release_device_grids() -> None:
     """Free the device grids cached between `execute` calls."""
     _GRIDS.clear()
+
+
+def stream_windows(extent: int, band: int, steps: int, r: int, windows: int | None = None) -> list:
+    """Windows of a streamed execute (see `_execute_streamed`): a list of
+    (slab_lo, slab_hi, win_lo, win_hi) in interior rows (2D) / planes (3D), or
+    [] when streaming does not pay.
+
+    The extent is cut into `windows` band-aligned slabs; window k is slab k
+    widened by the margin M = T*r rounded up to whole tile bands (clipped to
+    the grid).  After T steps the rows the window's frozen outer halo has
+    contaminated lie within T*r of the window edge, outside the slab, and the
+    band-aligned window keeps every tile where the whole-grid run has it, so
+    the slab comes out bit-identical.  Default count: 4 windows when the
+    extent is at least 16 margins (B9: 10240 rows, M = 128), fewer down to 2
+    above 8 margins, else none; SPD_STREAM_WINDOWS overrides."""
+    margin = -(-steps * r // band) * band
+    if windows is None:
+        env = os.environ.get("SPD_STREAM_WINDOWS")
+        windows = int(env) if env else min(4, extent // (4 * margin))
+    units = -(-extent // band)
+    windows = min(int(windows), units)
+    if windows < 2:
+        return []
+    out = []
+    for k in range(windows):
+        lo = units * k // windows * band
+        hi = min(extent, units * (k + 1) // windows * band)
+        out.append((lo, hi, max(0, lo - margin), min(extent, hi + margin)))
+    return out
+
+
+_STREAMS = threading.local()
+
+
+def _side_streams(device: int, n: int) -> list:
+    """n CUDA streams of `device` owned by this host thread (reused across
+    calls, so concurrent callers never share them)."""
+    cache = getattr(_STREAMS, "by_dev", None)
+    if cache is None:
+        cache = _STREAMS.by_dev = {}
+    lst = cache.setdefault(device, [])
+    while len(lst) < n:
+        lst.append(torch.cuda.Stream(device))
+    return lst[:n]
+
+
+def _execute_streamed(plan: Plan, kernel: StencilKernel, data: np.ndarray, halo: int, steps: int, windows: list,
+                      target: torch.Tensor) -> None:
+    """One-device execute with the host transfers overlapped with the steps.
+
+    Each window (`stream_windows`) is an independent grid: its upload (copy
+    stream), its T steps (compute stream) and the download of its slab rows
+    (second copy stream) are chained by events, so window k+1's upload and
+    window k-1's download run under window k's steps -- PCIe is full duplex
+    and the copy engines are separate from the SMs.  The price is the margin
+    rows every window recomputes; the result is bit-identical to the
+    whole-grid run.  `target`: the dense host result (pinned for overlap)."""
+    dense_shape = tuple(int(v) for v in data.shape)
+    row_elems = int(np.prod(dense_shape[1:]))
+    rest = tuple(v - 2 * halo for v in dense_shape[1:])
+    host_in = torch.from_numpy(data)
+    s_in, s_out, s_c = _side_streams(plan.device, 3)
+    caller = torch.cuda.current_stream()
+    for st in (s_in, s_out, s_c):
+        st.wait_stream(caller)
+    grids = []
+    try:
+        for k, (lo, hi, wl, wh) in enumerate(windows):
+            g = _GRIDS.acquire(plan, (wh - wl,) + rest, halo)
+            grids.append(g)
+            g.upload(host_in[wl : wh + 2 * halo], stream=s_in)
+            up = torch.cuda.Event()
+            up.record(s_in)
+            s_c.wait_event(up)
+            g.run(steps, stream=s_c)
+            done = torch.cuda.Event()
+            done.record(s_c)
+            s_out.wait_event(done)
+            a = 0 if k == 0 else lo - wl + halo
+            b = wh - wl + 2 * halo if k == len(windows) - 1 else hi - wl + halo
+            g.download_rows(target.data_ptr() + wl * row_elems * 2, a, b, stream=s_out)
+        caller.wait_stream(s_out)
+        s_out.synchronize()
+    finally:
+        for g in grids:
+            _GRIDS.release(g)
 
 
 def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=None):
@@ -364,6 +451,48 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
         stats.device["exchange"] = "peer memory (spd_slab_run), one slab per listed device"
         cls = Grid3D if kernel.d == 3 else Grid
         return cls(res, grid.halo, grid.step + steps), stats
+    with _InFlight(plan.device) as concurrent:
+        # Streamed windows pay off for a lone caller; with other calls in
+        # flight on the device their copies already overlap this call's
+        # steps, and the margin rows would only add work.
+        if native16 and kernel.d >= 2 and concurrent == 0:
+            band = plan.info().tile_z if kernel.d == 3 else plan.info().tile_y
+            windows = stream_windows(shape[0], band, steps, kernel.r)
+            if windows:
+                with torch.cuda.device(plan.device):
+                    target = torch.from_numpy(out.data) if out is not None else torch.empty(
+                        data.shape, dtype=torch.float16, pin_memory=True)
+                    _execute_streamed(plan, kernel, np.ascontiguousarray(data), grid.halo, steps, windows, target)
+                stats.device["streamed_windows"] = len(windows)
+                cls = Grid3D if kernel.d == 3 else Grid
+                return cls(target.numpy(), grid.halo, grid.step + steps), stats
+        return _execute_whole(plan, kernel, grid, steps, shape, native16, out, stats)
+
+
+class _InFlight:
+    """Counts execute() calls in flight per device; entering returns how many
+    other calls were running on it."""
+
+    _lock = threading.Lock()
+    _count: dict = {}
+
+    def __init__(self, device: int):
+        self.device = device
+
+    def __enter__(self) -> int:
+        with self._lock:
+            n = self._count.get(self.device, 0)
+            self._count[self.device] = n + 1
+        return n
+
+    def __exit__(self, *exc) -> None:
+        with self._lock:
+            self._count[self.device] -= 1
+
+
+def _execute_whole(plan: Plan, kernel: StencilKernel, grid, steps: int, shape, native16: bool, out, stats):
+    """Whole-grid execute: upload, T steps, download on the current stream."""
+    data = grid.data
     with torch.cuda.device(plan.device):
         dg = _GRIDS.acquire(plan, shape, grid.halo)
         try:
@@ -484,5 +613,6 @@ __all__ = [
     "get_plan",
     "exec_stats",
     "release_device_grids",
+    "stream_windows",
     "DEFAULT_TOLERANCE",
 ]

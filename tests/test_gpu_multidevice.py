@@ -68,3 +68,29 @@ def test_multidevice_rejects_too_many_slabs():
     g = _grid(2, 1, (64, 512), np.float16)  # two 32-row bands
     with pytest.raises(ValueError):
         sp.execute(k, g, 2, DeviceConfig(devices=(0, 0, 0)))
+
+
+@gpu
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("d,r,shape,steps,halo,windows", [
+    (2, 1, (512, 1024), 4, 1, None),      # default: 4 windows
+    (2, 1, (1000, 512), 7, 1, 3),         # ragged extent
+    (2, 3, (384, 1024), 3, 3, None),
+    (2, 1, (256, 512), 2, 2, 2),          # grid halo > r
+    (3, 1, (64, 32, 256), 2, 1, None),    # 3D: staged window uploads
+])
+def test_streamed_execute_matches_whole_grid(monkeypatch, d, r, shape, steps, halo, windows):
+    k = _kernel(d, r)
+    rng = np.random.default_rng([7, *shape])
+    data = rng.uniform(-1, 1, tuple(s + 2 * halo for s in shape)).astype(np.float16)
+    g = sp.Grid3D(data, halo) if d == 3 else sp.Grid(data, halo)
+    monkeypatch.setenv("SPD_STREAM_WINDOWS", "0")
+    want, st0 = sp.execute(k, g, steps)
+    assert "streamed_windows" not in st0.device
+    monkeypatch.setenv("SPD_STREAM_WINDOWS", str(windows) if windows else "")
+    if windows is None:
+        monkeypatch.delenv("SPD_STREAM_WINDOWS")
+    for _ in range(2):
+        got, st = sp.execute(k, g, steps)
+        assert st.device["streamed_windows"] >= 2
+        assert np.array_equal(got.data, want.data)
