@@ -134,6 +134,12 @@ int spd_plan_operands(const spd_plan* plan, uint16_t* a_img, uint32_t* e_words,
 /* Tile geometry tables: in_off[3*R_in] = (dz, dy, dx) of each input image row
  * relative to the tile origin, out_off[3*R_out*max(m_tiles, 2*cg2)] likewise for output rows. */
 int spd_plan_geometry(const spd_plan* plan, int32_t* in_off, int32_t* out_off);
+/* MMA row / accumulator TMEM lane of each logical kernel-matrix row
+ * m = L*a + i (output row a of the M-tile, position i in the x-chunk);
+ * lane[m] for m < r_out*L.  2D / 1D r = 1 plans use the quad-pair order read
+ * back by the epilogue's tcgen05.ld.16x256b; 3D and other radii the
+ * identity. */
+int spd_plan_lane_map(const spd_plan* plan, int32_t* lane);
 
 /* ---------------------------------------------------------------------------
  * Device grid layout.  Interior (z, y, x) lives at element

@@ -297,6 +297,11 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
     return set_error(SPD_EINVAL, "dimensionality must be 1, 2 or 3, got %d", d);
   }
   g->r_in = rin;
+  // L = 4, one M-tile (2D, 1D): quad-pair lane map (see Geometry::lane_map
+  // and the epilogue).  The 3D two-M-tile geometry keeps the linear map: its
+  // quad-pair epilogue measured 123.8 -> 141.9 us per B27 step, while 2D r = 1
+  // gains ~1 % (B9 79.3 -> 78.4 us; profiles/r02_epilogue.txt).
+  g->lane_map = (L == 4 && g->m_tiles == 1 && !g->cg2) ? 1 : 0;
   // B image: core matrices (8 chunks x 16 B) of consecutive window K-chunks
   // are adjacent (LBO = 128 B); 8-chunk groups are SBO apart.  UMMA needs the
   // core matrices 128-B aligned, so SBO is a multiple of 128.
@@ -316,6 +321,12 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   g->s = s;
   if (s > SPD_MAX_S) return set_error(SPD_EINVAL, "tile needs %d MMAs (max %d)", s, SPD_MAX_S);
   return SPD_OK;
+}
+
+// MMA row (= accumulator TMEM lane) holding output row a, chunk position i.
+int lane_of(const Geometry& g, int a, int i) {
+  if (g.lane_map == 1) return 16 * (a / 4) + 2 * (a % 4) + (i >> 1) + 8 * (i & 1);
+  return g.L * a + i;
 }
 
 // Kernel-row index for an (input row, output row) pair, or -1 if the input row
@@ -361,7 +372,7 @@ int pack_operands(const Geometry& g, int n_rows, const double* row_values,
         const double* vals = row_values + (size_t)kr * L * L;
         const uint8_t* meta = row_meta + (size_t)kr * L * segs_per_row * 2;
         for (int i = 0; i < L; ++i) {
-          int m = L * a + i;
+          int m = lane_of(g, a, i);
           for (int sg = 0; sg < segs_per_row; ++sg) {
             int kseg = c * 2 * g.kc + sg;  // segment within K=32 (rows padded to kc chunks)
             for (int t = 0; t < 2; ++t) {

@@ -50,7 +50,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // Development builds only (tools/build_variant.sh <name> -DSPD_DEVEL): the
 // per-role timeline (SPD_TRACE, event e of tile-iteration it in CTAs 0-7) and
 // the role-elimination switches (SPD_DBG bits 1: no output stores, 4: no
-// producer work, 16: no epilogue transpose).  The production library compiles
+// producer work, 8: no MMAs, 16: no epilogue transpose).  The production library compiles
 // both to nothing: no runtime debug branch sits in a hot loop, and no switch
 // can remove a fence.
 #ifdef SPD_DEVEL
@@ -211,6 +211,18 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
         "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+// 16 lanes x 256 bits, four repetitions (32 columns): thread t receives
+// {D[l][c], D[l][c+1], D[l+8][c], D[l+8][c+1]} for l = t/4 and columns
+// c = 8k + 2(t%4), k = 0..3, in that register order (tools/tmem_layout.cu).
+__device__ __forceinline__ void tmem_ld_16x256b_x4(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
 
@@ -1132,6 +1144,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           const int start = (s * RPM + RPM <= RIN_MMA ? s * RPM : RIN_MMA - RPM) + mt * MTR;
           // descriptor start address field is addr >> 4
           const uint64_t bdesc = bdesc0 + (uint64_t)((start * KC * 128) >> 4);
+          if (SPD_DBG_BIT(8)) continue;  // role elimination (SPD_DEVEL builds only)
           if constexpr (CG2)
             mma_sp_ts_elect_cg2(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
           else
@@ -1257,6 +1270,140 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
         }
       }
      }
+    } else if constexpr (C::CPL == 2 && MT == 1 && !CG2) {
+    // L = 4, quad-pair lane map (aot.cpp lane_of): accumulator lane
+    // 16 s + 2 rho + (i >> 1) + 8 (i & 1) holds output row 4 s + rho, chunk
+    // position i.  Warp `quad` drains the 16-lane slabs s = 2 quad + h
+    // (h = 0, 1) with tcgen05.ld.16x256b: thread t gets lanes 16 s + t/4
+    // (position 2 hi, hi = bit 2 of t) and + 8 (position 2 hi + 1), i.e. one
+    // packed word of two consecutive x per chunk, for columns 8k + 2 (t & 3)
+    // + {0, 1}.  Under the sigma column order the four columns of a 16-column
+    // block give the thread the four consecutive chunks 4 (t & 3) + 0..3 of
+    // that block; thread t ^ 4 holds the other two positions of the same
+    // chunks.  One xor-4 shuffle per chunk then leaves each thread all four
+    // positions of its four chunks in one block of the 32-column batch (block
+    // `hi`): 32 contiguous bytes, one 256-bit store, and each warp store
+    // instruction covers whole 128-byte lines.  (The 32x32b read of a linear
+    // lane map needed a two-level 4-lane butterfly: ~8.5 instructions per
+    // output word against ~3 here.)
+    const int quad = warp % 4;
+    const int grp = warp / 4;
+    const int rho = lane >> 3;             // row within the slab
+    const bool hi = ((lane >> 2) & 1) != 0;  // positions 2, 3 (else 0, 1); stores block 1 of a batch
+    const int cq = lane & 3;               // column pair within each 8-column group
+    // output row of this thread in slab h of M-tile mt (M-tile t holds rows a + t*R_OUT)
+    int odz[MT][2], ody[MT][2], odx[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = 4 * (2 * quad + h) + rho + (mt + (int)crank) * C::R_OUT;
+        odz[mt][h] = g.out_dz[a];
+        ody[mt][h] = g.out_dy[a];
+        odx[mt][h] = g.out_dx[a];
+      }
+    int it = 0;
+    int pit = 0;  // published tiles (publish ring index)
+    int2 e_nx = fetch(wid0);
+    int e_gi = wid0;
+    for (int gi = wid0; gi < total; gi += wstride, ++it) {
+      if (kEpiGroups > 1 && (it % kEpiGroups) != grp) continue;
+      const int acc = it % NACC;
+      const uint32_t aphase = (it / NACC) & 1;
+      const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
+      e_nx = fetch(gi + wstride);
+      e_gi = gi + wstride;
+      const TileId id = decode_e(gi, e_cur);
+      T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
+      bool row_ok[MT][2];
+      int64_t chunk_lim[MT][2];  // valid chunks in this row
+      T* orow[MT][2];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t z = id.z0 + odz[mt][h];
+          const int64_t y = id.y0 + ody[mt][h];
+          const int64_t xr = id.x0 + odx[mt][h];  // x of chunk 0 of this row
+          if (g.d == 3) row_ok[mt][h] = z >= p.row_lo && z < p.row_hi && y < p.ny;
+          else if (g.d == 2) row_ok[mt][h] = y >= p.row_lo && y < p.row_hi;
+          else row_ok[mt][h] = true;
+          chunk_lim[mt][h] = (p.nx - xr) / L;
+          orow[mt][h] = out + p.origin + z * p.plane + y * p.pitch + xr;
+        }
+      if (warp == 0 && lane == 0) SPD_TRACE(12, it);
+      mbar_wait(bar_accf + 8 * acc, aphase);
+      tc_fence_after();
+      if (warp == 0 && lane == 0) SPD_TRACE(8, it);
+      constexpr int NB = C::ACC_STAGE / MT / 32;  // 32-column batches per M-tile (pair: both x-halves)
+      constexpr int TB = MT * NB;                 // batch bi: M-tile bi / NB, column batch bi % NB
+      const uint32_t tcol = tmem + ((uint32_t)(quad * 32) << 16) + C::ACC_COL + acc * C::ACC_STAGE;
+      auto load = [&](int bi, uint32_t(&v)[2][16]) {
+        tmem_ld_16x256b_x4(tcol + 32 * bi, v[0]);
+        tmem_ld_16x256b_x4(tcol + (16u << 16) + 32 * bi, v[1]);
+      };
+      auto emit = [&](int bi, const uint32_t(&v)[2][16]) {
+        const int mt = bi / NB, cb = bi % NB;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          // w[b][j]: block b of the batch, chunk 4 cq + j, positions (2 hi, 2 hi + 1)
+          uint32_t w[2][4];
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int k = 2 * b + (j & 1), e = j >> 1;
+              w[b][j] = Cvt<T>::pack(__uint_as_float(v[h][4 * k + e]), __uint_as_float(v[h][4 * k + 2 + e]));
+            }
+          uint32_t o[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t r = __shfl_xor_sync(0xffffffffu, hi ? w[0][j] : w[1][j], 4);
+            o[2 * j] = hi ? r : w[0][j];
+            o[2 * j + 1] = hi ? w[1][j] : r;
+          }
+          if (!row_ok[mt][h] || SPD_DBG_BIT(1)) continue;
+          const int64_t ch0 = (int64_t)cb * 32 + (hi ? 16 : 0) + 4 * cq;
+          T* dst = orow[mt][h] + ch0 * L;
+          if (ch0 + 4 <= chunk_lim[mt][h]) {
+            stg_v8(dst, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (ch0 + c < chunk_lim[mt][h]) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(o[2 * c], o[2 * c + 1]);
+          }
+        }
+      };
+      uint32_t va[2][16], vb[2][16];
+      load(0, va);
+      tmem_wait_ld();
+#pragma unroll
+      for (int bi = 0; bi < TB; ++bi) {
+        uint32_t(&cur)[2][16] = (bi & 1) ? vb : va;
+        uint32_t(&nxt)[2][16] = (bi & 1) ? va : vb;
+        if (bi + 1 < TB) load(bi + 1, nxt);
+        if (bi == TB - 1) {
+          // every accumulator column is in registers: free the stage
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG2 && crank != 0) mbar_arrive_cluster(bar_acce + 8 * acc, 0);
+            else mbar_arrive(bar_acce + 8 * acc);
+          }
+        }
+        if (warp == 0 && lane == 0 && bi == 0) SPD_TRACE(10, it);
+        emit(bi, cur);
+        if (bi + 1 < TB) tmem_wait_ld();
+      }
+      if (warp == 0 && lane == 0) SPD_TRACE(9, it);
+      if (publishing && pub_tile(id) && !SPD_DBG_BIT(2048)) {
+        const int ps = pit % kNPub;
+        mbar_wait(bar_pube + 8 * ps, ((pit / kNPub) & 1) ^ 1);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
+        ++pit;
+      }
+    }
     } else {
     const int quad = warp % 4;       // TMEM lane quadrant (warp id mod 4)
     const int grp = warp / 4;        // epilogue group: tiles it == grp (mod kEpiGroups)
@@ -1643,6 +1790,8 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
   if (CG2 != (plan->g.cg2 != 0)) return set_error(SPD_EUNSUPPORTED, "CTA-pair geometry mismatch");
   auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
+  if ((C::CPL == 2 && !C::GEN && MT == 1 && !CG2) != (plan->g.lane_map == 1))
+    return set_error(SPD_EUNSUPPORTED, "accumulator lane map mismatch (%d)", plan->g.lane_map);
   {  // the MMA issuer's compile-time schedule must be the plan's
     constexpr int RPM = 4 / C::KC;
     constexpr int RM = C::RIN_MMA;
@@ -2078,6 +2227,14 @@ int spd_plan_operands(const spd_plan* plan, uint16_t* a_img, uint32_t* e_words, 
   if (e_words) std::memcpy(e_words, plan->e_words.data(), plan->e_words.size() * sizeof(uint32_t));
   if (start_rows)
     for (int s = 0; s < plan->g.s; ++s) start_rows[s] = plan->g.start_row[s];
+  return SPD_OK;
+}
+
+int spd_plan_lane_map(const spd_plan* plan, int32_t* lane) {
+  if (!plan || !lane) return spd::set_error(SPD_EINVAL, "null argument");
+  const spd::Geometry& g = plan->g;
+  for (int a = 0; a < g.r_out; ++a)
+    for (int i = 0; i < g.L; ++i) lane[g.L * a + i] = spd::lane_of(g, a, i);
   return SPD_OK;
 }
 

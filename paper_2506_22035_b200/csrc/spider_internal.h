@@ -43,6 +43,9 @@ struct Geometry {
   int mt_rows;       // input-row offset between consecutive M-tiles
   int cg2;           // 3D CTA-pair mode: one M = 256 tcgen05.mma.sp.cta_group::2 per K-block;
                      // CTA rank t holds output rows t*r_out.. (its own A/E images) and x-half t of B
+  int lane_map;      // MMA row (TMEM lane) of output row a, chunk position i: 0 linear (m = L*a + i);
+                     // 1 quad pair (L = 4, one M-tile): m = 16*(a/4) + 2*(a%4) + (i>>1) + 8*(i&1), read back
+                     // with tcgen05.ld.16x256b (lanes m and m+8 land in one thread: phases i, i+1)
   int r_in;          // input image rows per tile
   int s;             // MMAs per tile
   int n_tile;        // x-chunks per tile (MMA N)
@@ -55,6 +58,7 @@ struct Geometry {
 };
 
 int build_geometry(int d, int r, int flags, Geometry* g);
+int lane_of(const Geometry& g, int a, int i);
 int pack_operands(const Geometry& g, int n_rows, const double* row_values,
                   const uint8_t* row_meta, int dtype, std::vector<uint16_t>& a_img,
                   std::vector<uint32_t>& e_words);

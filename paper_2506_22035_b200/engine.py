@@ -122,6 +122,14 @@ class Plan:
         check(lib.spd_plan_geometry(self._h, i32ptr(a), i32ptr(b)))
         return a, b
 
+    def lane_map(self) -> np.ndarray:
+        """MMA row (accumulator TMEM lane) of logical kernel-matrix row
+        m = L*a + i (output row a, chunk position i), length r_out*L."""
+        inf = self.info()
+        lanes = np.zeros(inf.r_out * inf.L, dtype=np.int32)
+        check(lib.spd_plan_lane_map(self._h, i32ptr(lanes)))
+        return lanes
+
     def layout(self, nz: int, ny: int, nx: int, halo: int) -> spd_grid_desc:
         desc = spd_grid_desc()
         check(lib.spd_grid_layout(self._h, int(nz), int(ny), int(nx), int(halo), C.byref(desc)))

@@ -45,6 +45,7 @@ def tile_model(plan, dense, halo):
     L, n_tile = inf.L, inf.n_tile * (2 if inf.cg2 else 1)  # a CTA pair spans both x-halves
     a_img, e_words, starts = plan.operands()
     in_off, out_off = plan.geometry()
+    lanes = plan.lane_map()  # accumulator row of (output row a, chunk position i)
     perm = sp.input_row_permutation(L, plan.parity).mapping
     A = decode_A(a_img, e_words)
     dense3 = dense if dense.ndim == 3 else dense[None]
@@ -74,7 +75,7 @@ def tile_model(plan, dense, halo):
             dz, dy, dx = out_off[a + t * inf.r_out]
             for i in range(L):
                 for n in range(n_tile):
-                    out[(dz, dy, dx + n * L + i)] = D[L * a + i, n]
+                    out[(dz, dy, dx + n * L + i)] = D[lanes[L * a + i], n]
     return out
 
 
@@ -162,3 +163,21 @@ def test_unsupported_radius_rejected_by_device_plan():
     k3 = sp.make_kernel_3d("box", 2, np.ones(125))
     with pytest.raises(ValueError, match="unsupported"):
         Plan(k3, "even", "fp16", device=-1)
+
+
+def test_lane_map_is_a_permutation():
+    """L = 4 one-M-tile plans (2D, 1D) put output row a, chunk position i on
+    accumulator lane 16*(a/4) + 2*(a%4) + (i>>1) + 8*(i&1) (the epilogue's
+    tcgen05.ld.16x256b order); 3D and other radii keep m = L*a + i."""
+    for d, r in ((2, 1), (3, 1), (1, 1), (2, 3), (2, 2)):
+        c = np.ones((2 * r + 1,) * d)
+        kern = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
+        plan = Plan(kern, "even", "fp16", device=-1)
+        inf = plan.info()
+        lanes = plan.lane_map()
+        assert sorted(lanes) == list(range(inf.r_out * inf.L))
+        for a in range(inf.r_out):
+            for i in range(inf.L):
+                quad_pair = inf.L == 4 and inf.m_tiles == 1 and not inf.cg2
+                want = 16 * (a // 4) + 2 * (a % 4) + (i >> 1) + 8 * (i & 1) if quad_pair else inf.L * a + i
+                assert lanes[inf.L * a + i] == want

@@ -2,7 +2,8 @@
 
 After T steps of a radius-r stencil, a point depends only on inputs within
 r*T of it.  So for the bench configurations at their full sizes and step
-counts (B9 / B49 at 10240^2, B27 at 512^3, T = 100):
+counts (B9 / B49 at 10240^2, B27 at 512^3, W at 16384^2, B25 at 10240 x 10242,
+T = 100):
 
 * the device result on the full grid, restricted to an inner block, equals
   the device result on a crop holding that block plus an r*T margin
@@ -33,7 +34,7 @@ pytestmark = pytest.mark.gpu
 TOL_T100 = 2e-2
 
 
-@pytest.mark.parametrize("name,inner", [("B9", 64), ("B49", 32), ("B27", 16)])
+@pytest.mark.parametrize("name,inner", [("B9", 64), ("B49", 32), ("B27", 16), ("W", 64), ("B25", 32)])
 @pytest.mark.parametrize("where", ["centre", "corner"])
 @pytest.mark.timeout(600, method="thread")
 def test_light_cone_full_size(name, inner, where):
@@ -53,9 +54,13 @@ def test_light_cone_full_size(name, inner, where):
     del full
 
     # crop origin (dense index of its first halo point) tile-aligned with the
-    # full grid: 64 in x, 8 in y / z; the block sits `margin` points inside
+    # full grid (the tile's row and x-chunk positions fix each point's
+    # accumulation order); the block sits `margin` points inside
+    inf = plan.info()
+    tile_x = inf.n_tile * inf.L
+    tiles = ([inf.tile_z] if d == 3 else []) + [inf.tile_y]
     if where == "centre":
-        cs = [(n // 2) // 8 * 8 for n in shape[:-1]] + [(shape[-1] // 2) // 64 * 64]
+        cs = [(n // 2) // t * t for n, t in zip(shape[:-1], tiles)] + [(shape[-1] // 2) // tile_x * tile_x]
     else:
         cs = [0] * d                             # keeps the global halo as its own
     lo = [c + margin for c in cs] if where == "centre" else [0] * d

@@ -6,6 +6,7 @@ set -u
 TAG=${1:-r02a}; shift || true
 TESTS=${1:-1}; shift || true
 CONFIGS=${@:-B9 B27}
+FIRST=${CONFIGS%% *}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > $OUT/nvsmi_$TAG.txt 2>&1
@@ -18,5 +19,7 @@ for c in $CONFIGS; do
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_${c}_$TAG.csv python tools/prof_step.py $c 6 > /dev/null 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:spider_step -s 3 -c 1 -o $OUT/prof_${c}_$TAG -f python tools/prof_step.py $c 5 > $OUT/ncu_${c}_$TAG.log 2>&1; tail -1 $OUT/ncu_${c}_$TAG.log
   python tools/ncu_summary.py $OUT/prof_${c}_$TAG.ncu-rep > $OUT/ncusum_${c}_$TAG.txt 2>&1
+  # gpurun brings back <= 64 MiB: keep the full report of the first config only
+  [ "$c" = "$FIRST" ] || rm -f $OUT/prof_${c}_$TAG.ncu-rep
 done
 ls -la $OUT | tail -30
