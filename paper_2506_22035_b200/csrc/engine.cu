@@ -54,11 +54,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // both to nothing: no runtime debug branch sits in a hot loop, and no switch
 // can remove a fence.
 #ifdef SPD_DEVEL
+#ifndef SPD_NO_TRACE
 #define SPD_TRACE(e, it)                                                                                 \
   do {                                                                                                   \
     if (p.trace && blockIdx.x < 8 && (it) < 64) *(volatile unsigned long long*)&p.trace[(blockIdx.x * 16 + (e)) * 64 + (it)] = gtimer(); \
   } while (0)
-#define SPD_DBG_BIT(b) ((p.dbg & (b)) != 0)
+#else
+#define SPD_TRACE(e, it) \
+  do {                   \
+  } while (0)
+#endif
+#ifndef SPD_DBG_MASK
+#define SPD_DBG_MASK 0xffffffff  // which switches are live (variant builds isolate one site)
+#endif
+#define SPD_DBG_BIT(b) ((((unsigned)(SPD_DBG_MASK)) & (b)) != 0 && (p.dbg & (b)) != 0)
 #else
 #define SPD_TRACE(e, it) \
   do {                   \
@@ -367,6 +376,9 @@ struct StepParams {
 // 97.2 us; 4: 115, 6: 99.0, 7: 100.6).
 #ifndef SPD_3D_PW
 #define SPD_3D_PW 4
+#endif
+#ifndef SPD_PROD_GUARD
+#define SPD_PROD_GUARD 0
 #endif
 #ifndef SPD_L8_PW
 #define SPD_L8_PW 5
@@ -938,9 +950,24 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       uint4 cur[NQ];
       uint4 edge[NQ];  // segment-edge lanes: the neighbouring 16-B block (one predicated load)
       const bool l0 = lpos == 0, l31 = lpos == SW - 1;
+#if SPD_PROD_GUARD == 1
+      // per-tile opaque copy of the item predicates (no loop-invariant to unswitch on)
+      bool vq[NQ];
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        if (valid[q] && !SPD_DBG_BIT(4)) {
+        uint32_t v = valid[q] ? 1u : 0u;
+        if (q == NQ - 1) asm volatile("" : "+r"(v));
+        vq[q] = v != 0;
+      }
+#define SPD_VALID(q) vq[q]
+#elif SPD_PROD_GUARD == 2
+#define SPD_VALID(q) (valid[q] && (p.dbg & 4) == 0)
+#else
+#define SPD_VALID(q) valid[q]
+#endif
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (SPD_VALID(q) && !SPD_DBG_BIT(4)) {
           cur[q] = lds_v4(nbase + noff[q]);
           edge[q] = make_uint4(0, 0, 0, 0);
           lds_v4_if(edge[q], l0 || l31, nbase + (l0 ? poff[q] : xoff_n[q]));
@@ -952,7 +979,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       // phase 2: neighbour exchange, permutation, B-image stores
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        if (valid[q] && !SPD_DBG_BIT(4)) {
+        if (SPD_VALID(q) && !SPD_DBG_BIT(4)) {
           uint32_t ext[12];
           const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
 #pragma unroll
