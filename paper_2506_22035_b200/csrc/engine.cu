@@ -339,6 +339,7 @@ struct StepParams {
   int n_tiles;
   int reverse;               // step 0 traverses tiles last-to-first; steps alternate
   int dbg;                   // development switches (SPD_DBG; read only in -DSPD_DEVEL builds)
+  int item_fence;            // always 0: a uniform branch per 2D r = 1 producer item (see the producer)
   unsigned long long* trace; // debug timeline (CTA 0): [event][tile] globaltimer stamps, or null
   const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
   const uint32_t* e_words;   // [S][128]
@@ -376,9 +377,6 @@ struct StepParams {
 // 97.2 us; 4: 115, 6: 99.0, 7: 100.6).
 #ifndef SPD_3D_PW
 #define SPD_3D_PW 4
-#endif
-#ifndef SPD_PROD_GUARD
-#define SPD_PROD_GUARD 0
 #endif
 #ifndef SPD_L8_PW
 #define SPD_L8_PW 5
@@ -950,24 +948,19 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       uint4 cur[NQ];
       uint4 edge[NQ];  // segment-edge lanes: the neighbouring 16-B block (one predicated load)
       const bool l0 = lpos == 0, l31 = lpos == SW - 1;
-#if SPD_PROD_GUARD == 1
-      // per-tile opaque copy of the item predicates (no loop-invariant to unswitch on)
-      bool vq[NQ];
+      // 2D r = 1: each work item sits behind its own uniform branch on
+      // p.item_fence (always 0; the compiler cannot fold it; the test must be
+      // written inline in each item's `if` -- a bool computed once is merged
+      // into one block).  Without the branches
+      // ptxas hoists all neighbour shuffles of the tile's 9 items ahead of the
+      // first B-image store (one basic block), and the step measured 7 %
+      // slower (B9 78.4 -> 72.9 us, W 194 -> 182 with the branches); the 3D
+      // and r = 3 producers measured 10-25 % slower WITH them
+      // (profiles/r02_prodsched.txt), so they keep one block.
+#define SPD_ITEM_OK(q) (valid[q] && (C::HALF || L != 4 || p.item_fence == 0))
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        uint32_t v = valid[q] ? 1u : 0u;
-        if (q == NQ - 1) asm volatile("" : "+r"(v));
-        vq[q] = v != 0;
-      }
-#define SPD_VALID(q) vq[q]
-#elif SPD_PROD_GUARD == 2
-#define SPD_VALID(q) (valid[q] && (p.dbg & 4) == 0)
-#else
-#define SPD_VALID(q) valid[q]
-#endif
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        if (SPD_VALID(q) && !SPD_DBG_BIT(4)) {
+        if (SPD_ITEM_OK(q) && !SPD_DBG_BIT(4)) {
           cur[q] = lds_v4(nbase + noff[q]);
           edge[q] = make_uint4(0, 0, 0, 0);
           lds_v4_if(edge[q], l0 || l31, nbase + (l0 ? poff[q] : xoff_n[q]));
@@ -979,7 +972,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       // phase 2: neighbour exchange, permutation, B-image stores
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        if (SPD_VALID(q) && !SPD_DBG_BIT(4)) {
+        if (SPD_ITEM_OK(q) && !SPD_DBG_BIT(4)) {
           uint32_t ext[12];
           const uint32_t cw[4] = {cur[q].x, cur[q].y, cur[q].z, cur[q].w};
 #pragma unroll
