@@ -301,7 +301,7 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   // and the epilogue).  The 3D two-M-tile geometry keeps the linear map: its
   // quad-pair epilogue measured 123.8 -> 141.9 us per B27 step, while 2D r = 1
   // gains ~1 % (B9 79.3 -> 78.4 us; profiles/r02_epilogue.txt).
-  g->lane_map = (L == 4 && g->m_tiles == 1 && !g->cg2) ? 1 : 0;
+  g->lane_map = ((L == 4 || (L == 8 && SPD_L8_PAIRS)) && g->m_tiles == 1 && !g->cg2) ? 1 : 0;
   // B image: core matrices (8 chunks x 16 B) of consecutive window K-chunks
   // are adjacent (LBO = 128 B); 8-chunk groups are SBO apart.  UMMA needs the
   // core matrices 128-B aligned, so SBO is a multiple of 128.
@@ -325,7 +325,10 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
 
 // MMA row (= accumulator TMEM lane) holding output row a, chunk position i.
 int lane_of(const Geometry& g, int a, int i) {
-  if (g.lane_map == 1) return 16 * (a / 4) + 2 * (a % 4) + (i >> 1) + 8 * (i & 1);
+  if (g.lane_map == 1) {  // 16-lane slabs of 16/L rows; lanes m, m+8 hold positions i, i+1
+    const int rows16 = 16 / g.L;
+    return 16 * (a / rows16) + (g.L / 2) * (a % rows16) + (i >> 1) + 8 * (i & 1);
+  }
   return g.L * a + i;
 }
 
