@@ -447,8 +447,13 @@ def run_ours(args, cfg_name):
         glob = (shape[0] * world,) + tuple(shape[1:])
         dense_shape = tuple(s + 2 * r for s in glob)
         devices = None if world == 1 else tuple(k % torch.cuda.device_count() for k in range(world))
-        e2e = e2e_rate(sp, make_kernel(kind, d, r), d, r, dense_shape, T, points_local * world,
-                       args.e2e_callers if world == 1 else 1, max(2, min(args.steps, 4)), devices)
+        try:
+            e2e = e2e_rate(sp, make_kernel(kind, d, r), d, r, dense_shape, T, points_local * world,
+                           args.e2e_callers if world == 1 else 1, max(2, min(args.steps, 4)), devices)
+        except Exception as exc:  # keep the device-timed line; say why e2e is missing
+            if world == 1:
+                raise
+            e2e = {"value": None, "unit": "GStencil/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

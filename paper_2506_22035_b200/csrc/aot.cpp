@@ -301,7 +301,9 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   // and the epilogue).  The 3D two-M-tile geometry keeps the linear map: its
   // quad-pair epilogue measured 123.8 -> 141.9 us per B27 step, while 2D r = 1
   // gains ~1 % (B9 79.3 -> 78.4 us; profiles/r02_epilogue.txt).
-  g->lane_map = ((L == 4 || (L == 8 && SPD_L8_PAIRS)) && g->m_tiles == 1 && !g->cg2) ? 1 : 0;
+  // (The same layout for L = 8 -- 16x256b reads plus a two-level butterfly
+  // over lanes ^4, ^8 -- measured B49 97.4 -> 108.0 us: not used.)
+  g->lane_map = (L == 4 && g->m_tiles == 1 && !g->cg2) ? 1 : 0;
   // B image: core matrices (8 chunks x 16 B) of consecutive window K-chunks
   // are adjacent (LBO = 128 B); 8-chunk groups are SBO apart.  UMMA needs the
   // core matrices 128-B aligned, so SBO is a multiple of 128.

@@ -1439,119 +1439,6 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
         ++pit;
       }
     }
-    } else if constexpr (L == 8 && SPD_L8_PAIRS && MT == 1 && !CG2) {
-    // L = 8, pair lane map (aot.cpp lane_of): slab s (16 lanes) holds output
-    // rows 2s, 2s+1; lane 16 s + 4 rho + pp (+ 8) holds positions 2 pp (+ 1)
-    // of row 2 s + rho.  tcgen05.ld.16x256b gives thread t (rho = t >> 4,
-    // pp = (t >> 2) & 3, c = t & 3) one packed word (positions 2pp, 2pp+1)
-    // of chunks 8k + 2c + {0, 1} for k = 0..3 of a 32-column batch.  A
-    // two-level xor butterfly over pp (lanes ^4, ^8) on 2-word units leaves
-    // thread pp all eight positions of chunks 8 pp + 2c + {0, 1}: 32
-    // contiguous bytes, one 256-bit store; a row's 16 threads cover 512 B.
-    const int quad = warp % 4;
-    const int grp = warp / 4;
-    const int rho = lane >> 4;
-    const int pp = (lane >> 2) & 3;
-    const int cq = lane & 3;
-    int ody[2], odx[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int a = 2 * (2 * quad + h) + rho + (int)crank * C::R_OUT;
-      ody[h] = g.out_dy[a];
-      odx[h] = g.out_dx[a];
-    }
-    int it = 0;
-    int pit = 0;
-    int2 e_nx = fetch(wid0);
-    int e_gi = wid0;
-    for (int gi = wid0; gi < total; gi += wstride, ++it) {
-      if (kEpiGroups > 1 && (it % kEpiGroups) != grp) continue;
-      const int acc = it % NACC;
-      const uint32_t aphase = (it / NACC) & 1;
-      const int2 e_cur = e_gi == gi ? e_nx : fetch(gi);
-      e_nx = fetch(gi + wstride);
-      e_gi = gi + wstride;
-      const TileId id = decode_e(gi, e_cur);
-      T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
-      bool row_ok[2];
-      int64_t chunk_lim[2];
-      T* orow[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int64_t y = id.y0 + ody[h];
-        const int64_t xr = id.x0 + odx[h];
-        row_ok[h] = g.d == 2 ? (y >= p.row_lo && y < p.row_hi) : true;
-        chunk_lim[h] = (p.nx - xr) / L;
-        orow[h] = out + p.origin + y * p.pitch + xr;
-      }
-      mbar_wait(bar_accf + 8 * acc, aphase);
-      tc_fence_after();
-      constexpr int TB = C::ACC_STAGE / 32;
-      const uint32_t tcol = tmem + ((uint32_t)(quad * 32) << 16) + C::ACC_COL + acc * C::ACC_STAGE;
-      auto load = [&](int bi, uint32_t(&v)[2][16]) {
-        tmem_ld_16x256b_x4(tcol + 32 * bi, v[0]);
-        tmem_ld_16x256b_x4(tcol + (16u << 16) + 32 * bi, v[1]);
-      };
-      auto emit = [&](int cb, const uint32_t(&v)[2][16]) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          // U[k][e]: chunk 8k + 2cq + e, positions (2pp, 2pp+1)
-          uint32_t U[4][2];
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-#pragma unroll
-            for (int e = 0; e < 2; ++e)
-              U[k][e] = Cvt<T>::pack(__uint_as_float(v[h][4 * k + e]), __uint_as_float(v[h][4 * k + 2 + e]));
-          // transpose (thread pp, slot k) -> (thread k, slot pp) over lanes ^4, ^8
-#pragma unroll
-          for (int b = 1; b < 4; b <<= 1) {
-            const bool upper = (pp & b) != 0;
-#pragma unroll
-            for (int dd = 0; dd < 4; ++dd) {
-              if (dd & b) continue;
-#pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                const uint32_t sv = upper ? U[dd][e] : U[dd | b][e];
-                const uint32_t r = __shfl_xor_sync(0xffffffffu, sv, 4 * b);
-                if (upper) U[dd][e] = r;
-                else U[dd | b][e] = r;
-              }
-            }
-          }
-          if (!row_ok[h] || SPD_DBG_BIT(1)) continue;
-          const int64_t ch0 = (int64_t)cb * 32 + 8 * pp + 2 * cq;
-          T* dst = orow[h] + ch0 * L;
-          if (ch0 + 2 <= chunk_lim[h]) {
-            stg_v8(dst, U[0][0], U[1][0], U[2][0], U[3][0], U[0][1], U[1][1], U[2][1], U[3][1]);
-          } else if (ch0 < chunk_lim[h]) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(U[0][0], U[1][0], U[2][0], U[3][0]);
-          }
-        }
-      };
-      uint32_t va[2][16], vb[2][16];
-      load(0, va);
-      tmem_wait_ld();
-#pragma unroll
-      for (int bi = 0; bi < TB; ++bi) {
-        uint32_t(&cur)[2][16] = (bi & 1) ? vb : va;
-        uint32_t(&nxt)[2][16] = (bi & 1) ? va : vb;
-        if (bi + 1 < TB) load(bi + 1, nxt);
-        if (bi == TB - 1) {
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar_acce + 8 * acc);
-        }
-        emit(bi, cur);
-        if (bi + 1 < TB) tmem_wait_ld();
-      }
-      if (publishing && pub_tile(id) && !SPD_DBG_BIT(2048)) {
-        const int ps = pit % kNPub;
-        mbar_wait(bar_pube + 8 * ps, ((pit / kNPub) & 1) ^ 1);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_pubf + 8 * ps);
-        ++pit;
-      }
-    }
     } else {
     const int quad = warp % 4;       // TMEM lane quadrant (warp id mod 4)
     const int grp = warp / 4;        // epilogue group: tiles it == grp (mod kEpiGroups)
@@ -1938,7 +1825,7 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
   if (CG2 != (plan->g.cg2 != 0)) return set_error(SPD_EUNSUPPORTED, "CTA-pair geometry mismatch");
   auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
-  if (((L == 4 || (L == 8 && SPD_L8_PAIRS)) && !C::GEN && MT == 1 && !CG2) != (plan->g.lane_map == 1))
+  if ((L == 4 && MT == 1 && !CG2) != (plan->g.lane_map == 1))
     return set_error(SPD_EUNSUPPORTED, "accumulator lane map mismatch (%d)", plan->g.lane_map);
   {  // the MMA issuer's compile-time schedule must be the plan's
     constexpr int RPM = 4 / C::KC;

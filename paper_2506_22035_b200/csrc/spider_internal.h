@@ -12,10 +12,6 @@
 #define SPD_MAX_RIN 128
 #define SPD_MAX_ROUT 64
 #define SPD_MAX_S 32
-// 2D r = 3 (L = 8) with the pair lane map and the 16x256b epilogue
-#ifndef SPD_L8_PAIRS
-#define SPD_L8_PAIRS 0
-#endif
 
 namespace spd {
 
