@@ -98,6 +98,7 @@ class ClockSampler:
         self.device = device
         self.period = period
         self.sm, self.maxsm, self.reasons = [], [], set()
+        self.power, self.limit, self.bits = [], None, 0
         self._stop = threading.Event()
         self._thread = None
 
@@ -121,9 +122,13 @@ class ClockSampler:
                 self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
                 self.maxsm.append(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
                 bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.bits |= bits
                 for name, bit in self.REASONS.items():
                     if bits & bit:
                         self.reasons.add(name)
+                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                if self.limit is None:
+                    self.limit = nv.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
             except Exception:
                 pass
             time.sleep(self.period)
@@ -137,7 +142,9 @@ class ClockSampler:
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": "nvml"}
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.maxsm), "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "source": "nvml"}
+                "samples": len(self.sm), "source": "nvml",
+                "power_w": round(statistics.median(self.power), 1) if self.power else None,
+                "power_limit_w": self.limit, "reason_bits": hex(self.bits)}
 
 
 def measured_peaks():
