@@ -465,7 +465,12 @@ class LocalSlabs:
         """`steps` steps of the dense host grid `data` (halo included);
         returns the dense result (written into `out` when given)."""
         h = self.halo
-        res = out if out is not None else np.empty(data.shape, dtype=np.float16 if native16 else np.float64)
+        if out is not None:
+            res = out
+        elif native16:  # pinned: the per-slab downloads run asynchronously
+            res = torch.empty(data.shape, dtype=torch.float16, pin_memory=True).numpy()
+        else:
+            res = np.empty(data.shape, dtype=np.float64)
 
         def load(k):
             s, g, (cs, _) = self.slabs[k], self.grids[k], self.streams[k]
@@ -504,10 +509,10 @@ class LocalSlabs:
             if k == len(self.slabs) - 1:
                 hi = res.shape[0]
             if native16:
-                tmp = torch.empty(g.dense_shape, dtype=torch.float16, pin_memory=True)
-                g.download(tmp, stream=cs)
+                # only this slab's rows, straight into the result (pinned: async)
+                row_elems = int(np.prod(res.shape[1:]))
+                g.download_rows(res.ctypes.data + s.lo * row_elems * 2, lo - s.lo, hi - s.lo, stream=cs)
                 cs.synchronize()
-                res[lo:hi] = tmp.numpy()[lo - s.lo : hi - s.lo]
             else:
                 with torch.cuda.stream(cs):
                     part = g.to_dense_f64(stream=cs).cpu().numpy()
