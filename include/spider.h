@@ -202,6 +202,15 @@ int spd_step_ordered(const spd_plan* plan, const spd_grid_desc* g, const void* i
                      void* out, const void* order, int n_pairs,
                      unsigned int* band_done, int publish, void* stream);
 
+/* One step with both edge bands (first and last tile row / plane) first, then
+ * the interior forward (dir 0) or backward (dir 1); with publish, every edge
+ * tile bumps band_done[band] (system scope) when its stores are visible.
+ * The slab step's launch (spd_slab_step): the order is computed per tile,
+ * so it costs no more than a plain step. */
+int spd_step_edge_first(const spd_plan* plan, const spd_grid_desc* g,
+                        const void* in, void* out, int dir,
+                        unsigned int* band_done, int publish, void* stream);
+
 /* One step restricted to output rows [y_begin, y_end) (2D) or planes
  * [z_begin, z_end) (3D) — used by the slab driver to compute the boundary
  * bands before the halo exchange and the interior after. */

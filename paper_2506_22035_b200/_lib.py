@@ -79,6 +79,7 @@ SIGNATURES = {
     "spd_step_range": (_I, [_P, _DESC, _P, _P, _I64, _I64, _P]),
     "spd_step_edges": (_I, [_P, _DESC, _P, _P, _P]),
     "spd_step_ordered": (_I, [_P, _DESC, _P, _P, _P, _I, _P, _I, _P]),
+    "spd_step_edge_first": (_I, [_P, _DESC, _P, _P, _I, _P, _I, _P]),
     "spd_pack_grid": (_I, [_DESC, _I, _P, _P, _P]),
     "spd_unpack_grid": (_I, [_DESC, _I, _P, _P, _P]),
     "spd_upload": (_I, [_DESC, _P, _P, _P]),

@@ -334,7 +334,9 @@ struct StepParams {
   int stepmajor;             // persistent (steps > 1) in plain step-major order: work item gi is tile
                              // gi % n_tiles of step gi / n_tiles (no order array); every step
                              // traverses its tiles forward
-  int use_order;             // steps == 1 with a host-given band order (slab step: edge bands first)
+  int use_order;             // steps == 1 with a host-given band order
+  int edge_order;            // steps == 1: 1 / 2 = both edge bands first, then the interior forward /
+                             // backward (the slab step; computed per tile, no order array)
   int publish;               // steps == 1: publish finished tiles to band_done (system scope) for a
                              // copy engine waiting on them (peer exchange inside one launch)
   int chain;                 // chained one-step launches of a run (SPD_RUN_CHAINED): every tile is
@@ -714,7 +716,18 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     if (!ordered) {
       id.step = 0;
       id.dep_step = p.chain_t;
-      t = p.reverse ? p.n_tiles - 1 - gi : gi;
+      if (p.edge_order) {
+        // slab step: both edge bands first, then the interior forward
+        // (edge_order 1: 0, nb-1, 1 .. nb-2) or backward (2: nb-1, 0, nb-2 .. 1);
+        // arithmetic, so no role waits on a per-tile order lookup
+        const int slot = gi / p.per_band;
+        const int nb = p.n_bands;
+        const int band = p.edge_order == 1 ? (slot == 0 ? 0 : (slot == 1 ? nb - 1 : slot - 1))
+                                           : (slot == 0 ? nb - 1 : (slot == 1 ? 0 : nb - slot));
+        t = band * p.per_band + (gi - slot * p.per_band);
+      } else {
+        t = p.reverse ? p.n_tiles - 1 - gi : gi;
+      }
     } else if (p.stepmajor) {
       id.step = gi / p.n_tiles;
       id.dep_step = id.step;
@@ -2401,6 +2414,25 @@ int spd_step_ordered(const spd_plan* plan, const spd_grid_desc* gd, const void* 
   sp.use_order = 1;
   sp.order = (const int2*)order;
   sp.total = n_pairs * sp.per_band;
+  sp.publish = publish ? 1 : 0;
+  sp.band_done = band_done;
+  return dispatch(plan, sp, (cudaStream_t)stream);
+}
+
+int spd_step_edge_first(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int dir,
+                        unsigned int* band_done, int publish, void* stream) {
+  using namespace spd;
+  int rc = check_desc(plan, gd);
+  if (rc) return rc;
+  if (plan->d == 1) return set_error(SPD_EINVAL, "band orders are defined for 2D / 3D grids");
+  if (plan->g.cg2) return set_error(SPD_EUNSUPPORTED, "edge-first launch not supported in CTA-pair mode");
+  if (dir != 0 && dir != 1) return set_error(SPD_EINVAL, "interior direction must be 0 or 1, got %d", dir);
+  if (publish && !band_done) return set_error(SPD_EINVAL, "publishing needs band counters");
+  const int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
+  StepParams sp;
+  rc = fill_step_params(plan, gd, in, out, 0, extent, 1, sp);
+  if (rc) return rc;
+  sp.edge_order = dir + 1;
   sp.publish = publish ? 1 : 0;
   sp.band_done = band_done;
   return dispatch(plan, sp, (cudaStream_t)stream);

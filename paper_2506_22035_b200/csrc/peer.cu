@@ -83,11 +83,11 @@ struct spd_slab {
   unsigned int* my_flags; // [0] from up, [1] from down (written by the neighbours)
   unsigned int wait_flags;
   cudaEvent_t boundary_done;
-  // one launch per step: edge bands first, published per band; the copy
-  // engine waits on the edge bands' counters instead of a kernel boundary
+  // one launch per step (spd_step_edge_first): edge bands first, published
+  // per band, then the interior forward (even steps) / backward (odd steps,
+  // L2 reuse); the copy engine waits on the edge bands' counters instead of
+  // a kernel boundary
   int n_bands, per_band;
-  int2* order = nullptr;             // device: 2 x n_bands {0, band}: edge bands first, then the
-                                     // interior forward (even steps) / backward (odd steps, L2 reuse)
   unsigned int* band_done = nullptr; // device: cumulative finished tiles per band
 };
 
@@ -184,16 +184,7 @@ int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, vo
     const int64_t tiles_y = g->dims == 3 ? (g->ny + info[6] - 1) / info[6] : 1;
     s->per_band = (int)(tiles_x * tiles_y);
     s->n_bands = (int)((s->extent + s->band - 1) / s->band);
-    std::vector<int2> ord;
-    for (int dir = 0; dir < 2; ++dir) {
-      const int first = dir ? s->n_bands - 1 : 0, second = dir ? 0 : s->n_bands - 1;
-      ord.push_back(make_int2(0, first));
-      if (s->n_bands > 1) ord.push_back(make_int2(0, second));
-      for (int k = 1; k < s->n_bands - 1; ++k) ord.push_back(make_int2(0, dir ? s->n_bands - 1 - k : k));
-    }
-    rc = rt_err(cudaMalloc(&s->order, sizeof(int2) * ord.size()), "order alloc");
-    if (!rc) rc = rt_err(cudaMemcpy(s->order, ord.data(), sizeof(int2) * ord.size(), cudaMemcpyHostToDevice), "order");
-    if (!rc) rc = rt_err(cudaMalloc(&s->band_done, sizeof(unsigned int) * s->n_bands), "counter alloc");
+    rc = rt_err(cudaMalloc(&s->band_done, sizeof(unsigned int) * s->n_bands), "counter alloc");
     if (!rc) rc = rt_err(cudaMemset(s->band_done, 0, sizeof(unsigned int) * s->n_bands), "counter reset");
     if (rc) return spd_slab_destroy(s), rc;
   }
@@ -204,7 +195,6 @@ int spd_slab_create(const spd_plan* plan, const spd_grid_desc* g, void* buf0, vo
 int spd_slab_destroy(spd_slab* s) {
   if (!s) return SPD_OK;
   cudaEventDestroy(s->boundary_done);
-  if (s->order) cudaFree(s->order);
   if (s->band_done) cudaFree(s->band_done);
   delete s;
   return SPD_OK;
@@ -235,9 +225,17 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
   }
   // 2a. one launch, edge bands first and published per band; the copy engine
   //     starts on the edge rows while the interior is still being computed
-  static const char* two_launch = getenv("SPD_SLAB_TWO_LAUNCH");
+  // Launch form (tools/ordered_time.py, cooled and interleaved, 1 B200; step
+  // time vs a plain step): one edge-first launch publishing its edge tiles
+  // costs B9 +4.9 %, W +4.7 %, B27 +25 % (system-scope publishing of 512
+  // edge tiles); an edge launch + an interior launch costs B9 +8.3 %, W
+  // +3.1 %, B27 +3.8 %.  So: two launches for 3D and for large slabs, one
+  // launch for small 2D slabs.  SPD_SLAB_TWO_LAUNCH=0/1 overrides.
+  static const char* two_env = getenv("SPD_SLAB_TWO_LAUNCH");
+  const bool two_launch = two_env ? atoi(two_env) != 0
+                                  : (s->g.dims == 3 || (int64_t)s->per_band * s->n_bands >= 10000);
   if ((s->has_up || s->has_dn) && !two_launch) {
-    int rc0 = spd_step_ordered(s->plan, &s->g, in, out, s->order + (t & 1) * s->n_bands, s->n_bands, s->band_done, 1, cs);
+    int rc0 = spd_step_edge_first(s->plan, &s->g, in, out, t & 1, s->band_done, 1, cs);
     if (rc0) return rc0;
     const cuuint32_t target = (cuuint32_t)((int64_t)(t + 1) * s->per_band);
     const size_t bytes = (size_t)s->r * s->unit * 2;

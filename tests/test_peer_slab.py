@@ -68,14 +68,19 @@ def _worker(rank, world, port, d, r, shape, steps, outdir):
 
 
 @pytest.mark.timeout(300, method="thread")
-@pytest.mark.parametrize("d,r,shape,world,steps", [
-    (2, 1, (256, 1024), 2, 5),
-    (2, 1, (224, 512), 3, 4),    # ragged last slab
-    (2, 3, (96, 1024), 2, 3),
-    (3, 1, (48, 24, 256), 3, 3),
+@pytest.mark.parametrize("d,r,shape,world,steps,launch", [
+    (2, 1, (256, 1024), 2, 5, None),
+    (2, 1, (224, 512), 3, 4, None),    # ragged last slab
+    (2, 3, (96, 1024), 2, 3, None),
+    (3, 1, (48, 24, 256), 3, 3, None),
+    (2, 1, (256, 1024), 2, 5, "1"),    # edge launch + interior launch (large 2D slabs)
+    (3, 1, (48, 24, 256), 3, 3, "0"),  # one edge-first launch (small 2D slabs)
 ])
-def test_peer_slab_matches_single_grid(d, r, shape, world, steps):
+def test_peer_slab_matches_single_grid(monkeypatch, d, r, shape, world, steps, launch):
     import torch.multiprocessing as mp
+
+    if launch is not None:
+        monkeypatch.setenv("SPD_SLAB_TWO_LAUNCH", launch)
 
     import paper_2506_22035_b200 as sp
     from paper_2506_22035_b200.engine import DeviceGrid

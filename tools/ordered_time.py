@@ -23,19 +23,41 @@ for name in sys.argv[1:] or ["B9", "W", "B27"]:
     last = ((shape[0] - 1) // band) * band
     def plain():
         g.run(1)
-    def ordered():
+    def ordered(publish=1, ot=ordt):
         a, b = g.bufs[g.cur], g.bufs[1 - g.cur]
         check(lib.spd_step_ordered(plan.handle, C.byref(g.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                                   C.c_void_p(ordt[par[0] * nb:].data_ptr()), nb, C.c_void_p(cnt.data_ptr()), 1, _stream_ptr()))
+                                   C.c_void_p(ot[par[0] * nb:].data_ptr()), nb, C.c_void_p(cnt.data_ptr()), publish,
+                                   _stream_ptr()))
+        par[0] ^= 1
+        g.flip()
+    # plain traversal order through the ordered launch (isolates the order array / publishing)
+    plain_order = list(range(nb)) + list(range(nb - 1, -1, -1))
+    plain_ordt = torch.tensor([[0, b] for b in plain_order], dtype=torch.int32, device="cuda")
+    def edge_first(publish=1):
+        a, b = g.bufs[g.cur], g.bufs[1 - g.cur]
+        check(lib.spd_step_edge_first(plan.handle, C.byref(g.desc), C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                      par[0], C.c_void_p(cnt.data_ptr()), publish, _stream_ptr()))
         par[0] ^= 1
         g.flip()
     def two():
         g.step_edges(); g.step_range(band, last); g.flip()
+    import time
+    variants = ((plain, "plain"), (ordered, "one launch, order array, published"),
+                (lambda: ordered(0), "one launch, order array, not published"),
+                (lambda: ordered(0, plain_ordt), "one launch, plain band order array, not published"),
+                (edge_first, "edge-first (arithmetic order), published"),
+                (lambda: edge_first(0), "edge-first (arithmetic order), not published"),
+                (two, "edges + interior launches"))
+    res = {lab: [] for _, lab in variants}
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for fn, lab in ((plain, "plain"), (ordered, "one launch, edges first, published"), (two, "edges + interior launches")):
-        for _ in range(5): fn()
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(50): fn()
-        e1.record(); torch.cuda.synchronize()
-        print(f"{name} {lab}: {e0.elapsed_time(e1) / 50 * 1e3:.1f} us/step", flush=True)
+    for rnd in range(3):  # interleaved rounds, each after a cool-down (sustained runs hit the power cap)
+        for fn, lab in variants:
+            time.sleep(1.0)
+            for _ in range(4): fn()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(20): fn()
+            e1.record(); torch.cuda.synchronize()
+            res[lab].append(e0.elapsed_time(e1) / 20 * 1e3)
+    for _, lab in variants:
+        print(f"{name} {lab}: {min(res[lab]):.1f} us/step (best of 3 x 20 after cool-down)", flush=True)
