@@ -453,8 +453,9 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
         return cls(res, grid.halo, grid.step + steps), stats
     with _InFlight(plan.device) as concurrent:
         # Streamed windows pay off for a lone caller; with other calls in
-        # flight on the device their copies already overlap this call's
-        # steps, and the margin rows would only add work.
+        # flight on the device (now or within the last second) their copies
+        # already overlap this call's steps, and the margin rows would only
+        # add work.
         if native16 and kernel.d >= 2 and concurrent == 0:
             band = plan.info().tile_z if kernel.d == 3 else plan.info().tile_y
             windows = stream_windows(shape[0], band, steps, kernel.r)
@@ -470,24 +471,42 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
 
 
 class _InFlight:
-    """Counts execute() calls in flight per device; entering returns how many
-    other calls were running on it."""
+    """Counts execute() calls in flight per device.  Entering returns how many
+    other calls were running on it, or -1 when none is running now but calls
+    overlapped within the last QUIET seconds: a caller among several
+    concurrent ones (bench: three host threads, B9 whole-grid 1236-1255
+    GStencil/s aggregate) loses throughput when one of its calls streams
+    (1114-1217 with streaming allowed whenever a call found the device idle;
+    tools/e2e_var.py)."""
 
+    QUIET = 1.0
     _lock = threading.Lock()
     _count: dict = {}
+    _last_overlap: dict = {}
 
     def __init__(self, device: int):
         self.device = device
 
     def __enter__(self) -> int:
+        import time
+
+        now = time.monotonic()
         with self._lock:
             n = self._count.get(self.device, 0)
             self._count[self.device] = n + 1
+            if n > 0:
+                self._last_overlap[self.device] = now
+            elif now - self._last_overlap.get(self.device, -1e9) < self.QUIET:
+                n = -1
         return n
 
     def __exit__(self, *exc) -> None:
+        import time
+
         with self._lock:
             self._count[self.device] -= 1
+            if self._count[self.device] > 0:
+                self._last_overlap[self.device] = time.monotonic()
 
 
 def _execute_whole(plan: Plan, kernel: StencilKernel, grid, steps: int, shape, native16: bool, out, stats):
