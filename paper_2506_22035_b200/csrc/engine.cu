@@ -1997,6 +1997,11 @@ static int make_tensor_map(const spd_plan* plan, const spd_grid_desc* gd, const 
   sp.nbox = (row_elems + 255) / 256;
   sp.boxw = ((row_elems + sp.nbox - 1) / sp.nbox + 7) / 8 * 8;
   sp.box_slot = (int)roundup((int64_t)sp.boxw * 2 * g.r_in, 128);
+  // (The producer quarter-warp straddling a box boundary reads with a 2-way
+  // bank conflict -- ncu: 5 wavefronts instead of 4 per LDS.128 on B9.
+  // Skewing the box slots to continue the row's bank pattern is illegal:
+  // tensor-TMA shared destinations must be 128-byte aligned (misaligned
+  // address fault, r02).)
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return set_error(SPD_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const int64_t rows = gd->plane / gd->pitch;
