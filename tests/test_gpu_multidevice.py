@@ -94,3 +94,13 @@ def test_streamed_execute_matches_whole_grid(monkeypatch, d, r, shape, steps, ha
         got, st = sp.execute(k, g, steps)
         assert st.device["streamed_windows"] >= 2
         assert np.array_equal(got.data, want.data)
+
+
+@gpu
+@pytest.mark.timeout(300, method="thread")
+def test_multidevice_bf16_matches_one_device():
+    k = _kernel(2, 1)
+    g = _grid(2, 1, (256, 512), np.float64)
+    want, _ = sp.execute(k, g, 3, DeviceConfig(dtype="bf16"))
+    got, _ = sp.execute(k, g, 3, DeviceConfig(dtype="bf16", devices=(0, 0)))
+    assert np.array_equal(got.data, want.data)
