@@ -383,6 +383,9 @@ struct StepParams {
 #ifndef SPD_2D_NNAT
 #define SPD_2D_NNAT 4
 #endif
+#ifndef SPD_2D_NACC
+#define SPD_2D_NACC 3
+#endif
 #ifndef SPD_EPI_GROUPS
 #define SPD_EPI_GROUPS 1
 #endif
@@ -1924,7 +1927,7 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   //  stages, items per producer warp>; stage counts fill the 227 KB of smem
   // (scan in profiles/r01_tuning.txt).
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 34)
-    return launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, 3, 34>(plan, sp, st);
+    return launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, SPD_2D_NACC, 34>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
     return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40, false, SPD_3D_PW>(plan, sp, st);
