@@ -321,7 +321,29 @@ def release_device_grids() -> None:
     _GRIDS.clear()
 
 
-def stream_windows(extent: int, band: int, steps: int, r: int, windows: int | None = None) -> list:
+# Streamed-execute cost model (per point): PCIe copy of an fp16 point one way
+# (~55 GB/s pinned), one step of a point on the device (B9, full clock) and the
+# fill / drain / tail of one step launch (profiles/r02_l2_probe.txt).  It
+# reproduces the measured B9 window scan (profiles/r02_streamed_e2e.txt).
+_COPY_PS_PER_POINT = 36.0
+_STEP_PS_PER_POINT = 0.75
+_LAUNCH_OVERHEAD_PS = 4.7e6
+
+
+def _stream_gain(extent: int, row_points: int, margin: int, steps: int, windows: int) -> float:
+    """Modelled time saved (ps) by `windows` streamed windows over the
+    whole-grid path: the copies of all but the first upload and the last
+    download overlap the steps; every window recomputes its margin rows and
+    pays its own launch fill and drain."""
+    copies = 2 * extent * row_points * _COPY_PS_PER_POINT
+    saved = copies * (1 - 1 / windows)
+    margins = steps * 2 * margin * (windows - 1) * row_points * _STEP_PS_PER_POINT
+    launches = steps * (windows - 1) * _LAUNCH_OVERHEAD_PS
+    return saved - margins - launches
+
+
+def stream_windows(extent: int, band: int, steps: int, r: int, windows: int | None = None,
+                   row_points: int = 10240) -> list:
     """Windows of a streamed execute (see `_execute_streamed`): a list of
     (slab_lo, slab_hi, win_lo, win_hi) in interior rows (2D) / planes (3D), or
     [] when streaming does not pay.
@@ -331,14 +353,26 @@ def stream_windows(extent: int, band: int, steps: int, r: int, windows: int | No
     the grid).  After T steps the rows the window's frozen outer halo has
     contaminated lie within T*r of the window edge, outside the slab, and the
     band-aligned window keeps every tile where the whole-grid run has it, so
-    the slab comes out bit-identical.  Default count: 4 windows when the
-    extent is at least 16 margins (B9: 10240 rows, M = 128), fewer down to 2
-    above 8 margins, else none; SPD_STREAM_WINDOWS overrides."""
+    the slab comes out bit-identical.  The default count maximises the
+    modelled gain (`_stream_gain`, 2..8 windows, each at least two margins
+    tall) and streams only when that gain is over 5 % of the whole-grid
+    time; SPD_STREAM_WINDOWS overrides (B9, T = 100: 4 windows; 1000 steps:
+    none)."""
     margin = -(-steps * r // band) * band
+    units = -(-extent // band)
     if windows is None:
         env = os.environ.get("SPD_STREAM_WINDOWS")
-        windows = int(env) if env else min(4, extent // (4 * margin))
-    units = -(-extent // band)
+        if env:
+            windows = int(env)
+        else:
+            whole = 2 * extent * row_points * _COPY_PS_PER_POINT + steps * extent * row_points * _STEP_PS_PER_POINT
+            best, windows = 0.05 * whole, 0
+            for n in range(2, 9):
+                if extent // n < 2 * margin:
+                    break
+                g = _stream_gain(extent, row_points, margin, steps, n)
+                if g > best:
+                    best, windows = g, n
     windows = min(int(windows), units)
     if windows < 2:
         return []
@@ -458,7 +492,7 @@ def execute(kernel: StencilKernel, grid, steps: int, cfg=ExecConfig(), *, out=No
         # add work.
         if native16 and kernel.d >= 2 and concurrent == 0:
             band = plan.info().tile_z if kernel.d == 3 else plan.info().tile_y
-            windows = stream_windows(shape[0], band, steps, kernel.r)
+            windows = stream_windows(shape[0], band, steps, kernel.r, row_points=int(np.prod(shape[1:])))
             if windows:
                 with torch.cuda.device(plan.device):
                     target = torch.from_numpy(out.data) if out is not None else torch.empty(

@@ -73,9 +73,9 @@ def test_multidevice_rejects_too_many_slabs():
 @gpu
 @pytest.mark.timeout(300, method="thread")
 @pytest.mark.parametrize("d,r,shape,steps,halo,windows", [
-    (2, 1, (512, 1024), 4, 1, None),      # default: 4 windows
+    (2, 1, (4096, 4096), 8, 1, None),     # default window count from the cost model
     (2, 1, (1000, 512), 7, 1, 3),         # ragged extent
-    (2, 3, (384, 1024), 3, 3, None),
+    (2, 3, (384, 1024), 3, 3, 3),
     (2, 1, (256, 512), 2, 2, 2),          # grid halo > r
     (3, 1, (64, 32, 256), 2, 1, None),    # 3D: staged window uploads
 ])
