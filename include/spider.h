@@ -114,13 +114,18 @@ int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype,
  * (measured slower than the default two-M-tile CTA; kept for experiments).
  * The geometry depends only on (d, r, flags), never on the environment. */
 #define SPD_PLAN_CTA_PAIR 1
+/* SPD_PLAN_NO_EMBED: keep a radius-2 1D / 2D stencil on the generic L = 6
+ * path (by default it runs as radius 3 with a zero ring, on the L = 8 fast
+ * path). */
+#define SPD_PLAN_NO_EMBED 2
 int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype,
                        int device, int flags, spd_plan** out);
 int spd_plan_destroy(spd_plan* plan);
 
 /* Introspection of the packed operands (for the exact-layout tests).
- * info[0..10] = {L, R_in, R_out (per M-tile), S, n_tile, tile_z, tile_y, kchunks,
- * m_tiles, mt_rows, cg2}.  The tile has m_tiles M = 128 tiles; M-tile t reuses
+ * info[0..11] = {L, R_in, R_out (per M-tile), S, n_tile, tile_z, tile_y, kchunks,
+ * m_tiles, mt_rows, cg2, r_dev} (L and r_dev are the device geometry's: an
+ * embedded radius-2 stencil reports L = 8, r_dev = 3).  The tile has m_tiles M = 128 tiles; M-tile t reuses
  * the MMA schedule with the B rows shifted by t * mt_rows.  cg2 = 1: a CTA pair
  * runs one M = 256 MMA per K-block; rank t has its own A/E images (operands
  * then hold 2 * S records, rank-major) for output rows t * R_out .. and stages

@@ -1500,7 +1500,9 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       const TileId id = decode_e(gi, e_cur);
       T* out = static_cast<T*>(p.buf[(id.step + 1) & 1]);
       bool row_ok[MT];
-      int64_t chunk_lim[MT];  // valid chunks in this row
+      int64_t chunk_lim[MT];  // whole chunks in this row
+      int64_t x_lim[MT];      // valid points of this row from its chunk 0 (a partial last chunk:
+                              // an embedded radius-2 grid's width is a multiple of 6, not 8)
       T* orow[MT];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
@@ -1510,7 +1512,8 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
         if (g.d == 3) row_ok[mt] = z >= p.row_lo && z < p.row_hi && y < p.ny;
         else if (g.d == 2) row_ok[mt] = y >= p.row_lo && y < p.row_hi;
         else row_ok[mt] = true;
-        chunk_lim[mt] = (p.nx - xr) / L;
+        x_lim[mt] = p.nx - xr;
+        chunk_lim[mt] = x_lim[mt] / L;
         orow[mt] = out + p.origin + z * p.plane + y * p.pitch + xr;
       }
       if (warp == 0 && lane == 0) SPD_TRACE(12, it);
@@ -1575,6 +1578,12 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
               T* dc = orow[mt] + ch * L;
               if (L == 4) *reinterpret_cast<uint2*>(dc) = make_uint2(w[2 * c], w[2 * c + 1]);
               else *reinterpret_cast<uint4*>(dc) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+            } else if (ch * L < x_lim[mt]) {  // partial last chunk: point by point
+              uint16_t* dc = reinterpret_cast<uint16_t*>(orow[mt] + ch * L);
+              const int n = (int)(x_lim[mt] - ch * L);
+#pragma unroll
+              for (int e = 0; e < L; ++e)
+                if (e < n) dc[e] = (uint16_t)(w[(L / 2) * c + e / 2] >> (16 * (e & 1)));
             }
           }
         }
@@ -2206,7 +2215,7 @@ int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype
                        spd_plan** out) {
   using namespace spd;
   if (!out) return set_error(SPD_EINVAL, "null output pointer");
-  if (flags & ~SPD_PLAN_CTA_PAIR) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
+  if (flags & ~(SPD_PLAN_CTA_PAIR | SPD_PLAN_NO_EMBED)) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
   if ((flags & SPD_PLAN_CTA_PAIR) && d != 3) return set_error(SPD_EUNSUPPORTED, "CTA-pair plans are 3D only");
   *out = nullptr;
   if (d < 1 || d > 3) return set_error(SPD_EINVAL, "unsupported dimensionality %d", d);
@@ -2224,18 +2233,37 @@ int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype
   int span = 2 * r + 1;
   int ncoef = d == 1 ? span : (d == 2 ? span * span : span * span * span);
   p->coeffs.assign(coeffs, coeffs + ncoef);
-  p->n_rows = ncoef / span;
-  p->row_values.resize((size_t)p->n_rows * L * L);
-  p->row_meta.resize((size_t)p->n_rows * L * (L / 2) * 2);
+  // Radius 2 in 1D / 2D runs as radius 3 with the coefficients embedded in a
+  // zero ring: the L = 8 fast path (profiles/r02_embed.txt: B25 154 -> ~97
+  // us) instead of the generic L = 6 one.  The grid keeps its own halo and
+  // width rule (multiple of 6); the zero ring's reads land in the zero
+  // padding or the TMA's zero fill, and the epilogue masks the last partial
+  // 8-point chunk.  SPD_PLAN_NO_EMBED keeps the L = 6 path.
+  int r_dev = r;
+  std::vector<double> dev_coeffs(coeffs, coeffs + ncoef);
+  if (r == 2 && d <= 2 && !(flags & SPD_PLAN_NO_EMBED)) {
+    r_dev = 3;
+    const int sp7 = 7;
+    dev_coeffs.assign(d == 1 ? sp7 : sp7 * sp7, 0.0);
+    for (int i = 0; i < (d == 1 ? 1 : span); ++i)
+      for (int j = 0; j < span; ++j)
+        dev_coeffs[(size_t)(d == 1 ? 0 : i + 1) * sp7 + j + 1] = coeffs[(size_t)(d == 1 ? 0 : i) * span + j];
+  }
+  const int L_dev = band_rows(r_dev);
+  const int span_dev = 2 * r_dev + 1;
+  p->n_rows = (int)dev_coeffs.size() / span_dev;
+  p->row_values.resize((size_t)p->n_rows * L_dev * L_dev);
+  p->row_meta.resize((size_t)p->n_rows * L_dev * (L_dev / 2) * 2);
   for (int k = 0; k < p->n_rows; ++k) {
-    int rc = transform_row(r, parity, coeffs + (size_t)k * span, p->row_values.data() + (size_t)k * L * L,
-                           p->row_meta.data() + (size_t)k * L * L);
+    int rc = transform_row(r_dev, parity, dev_coeffs.data() + (size_t)k * span_dev,
+                           p->row_values.data() + (size_t)k * L_dev * L_dev,
+                           p->row_meta.data() + (size_t)k * L_dev * L_dev);
     if (rc) {
       delete p;
       return rc;
     }
   }
-  int rc = build_geometry(d, r, flags, &p->g);
+  int rc = build_geometry(d, r_dev, flags & ~SPD_PLAN_NO_EMBED, &p->g);
   if (rc) {
     delete p;
     return rc;
@@ -2290,6 +2318,7 @@ int spd_plan_info(const spd_plan* plan, int32_t* info) {
   info[8] = g.m_tiles;
   info[9] = g.mt_rows;
   info[10] = g.cg2;
+  info[11] = g.r;  // device radius (3 for an embedded radius-2 stencil)
   return SPD_OK;
 }
 
@@ -2372,7 +2401,7 @@ int spd_grid_layout(const spd_plan* plan, int64_t nz, int64_t ny, int64_t nx, in
   out->origin = zoff * out->plane + yoff * pitch + xoff;
   // + slack: the generic-radius row view may read a few elements past the
   // last padded row (boxes are rounded up to 8 elements)
-  out->alloc_elems = planes * out->plane + (plan->d == 2 && plan->L != 4 && plan->L != 8 ? 4096 : 0);
+  out->alloc_elems = planes * out->plane + (plan->d == 2 && plan->g.L != 4 && plan->g.L != 8 ? 4096 : 0);
   return SPD_OK;
 }
 

@@ -22,6 +22,7 @@ from .transform import Parity
 
 TORCH_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
 SPD_PLAN_CTA_PAIR = 1  # include/spider.h
+SPD_PLAN_NO_EMBED = 2
 SPD_RUN_PERSISTENT, SPD_RUN_CHAINED, SPD_RUN_FORWARD, SPD_RUN_STEPMAJOR = 1, 2, 4, 8  # include/spider.h
 # default spd_run_ex flags of DeviceGrid.run (one launch per step)
 RUN_FLAGS = 0
@@ -56,6 +57,7 @@ class PlanInfo:
     m_tiles: int = 1  # M = 128 tiles per tile (3D: 2, sharing one input block)
     mt_rows: int = 0  # input-row shift of M-tile t's MMA schedule: t * mt_rows
     cg2: int = 0      # CTA-pair mode (3D): rank t owns M-tile t and its own A/E images
+    r_dev: int = 0    # device radius (3 for a radius-2 stencil embedded in a zero ring)
 
 
 class Plan:
@@ -79,8 +81,11 @@ class Plan:
         self._coeffs = coeffs
         self.cta_pair = bool(cta_pair)
         h = C.c_void_p()
+        flags = SPD_PLAN_CTA_PAIR if cta_pair else 0
+        if os.environ.get("SPD_NO_EMBED"):  # development override: radius 2 on the generic L = 6 path
+            flags |= SPD_PLAN_NO_EMBED
         check(lib.spd_plan_create_ex(kernel.d, kernel.r, self.parity.code, dptr(coeffs), DTYPE_CODES[dtype],
-                                     self.device, SPD_PLAN_CTA_PAIR if cta_pair else 0, C.byref(h)))
+                                     self.device, flags, C.byref(h)))
         self._h = h
 
     @property
@@ -99,7 +104,7 @@ class Plan:
             pass
 
     def info(self) -> PlanInfo:
-        buf = np.zeros(11, dtype=np.int32)
+        buf = np.zeros(12, dtype=np.int32)
         check(lib.spd_plan_info(self._h, i32ptr(buf)))
         return PlanInfo(*[int(v) for v in buf])
 

@@ -183,7 +183,8 @@ def get_plan(kernel: StencilKernel, parity: Parity, dtype: str, device: int | No
     called from several host threads at once (each on its own current CUDA
     stream), as the reference's pure functions may."""
     dev = require_cuda(device).index if device is None else int(device)
-    key = (kernel.d, kernel.r, np.asarray(kernel.coeffs, dtype=np.float64).tobytes(), Parity(parity), dtype, dev)
+    key = (kernel.d, kernel.r, np.asarray(kernel.coeffs, dtype=np.float64).tobytes(), Parity(parity), dtype, dev,
+           bool(os.environ.get("SPD_NO_EMBED")))  # the plan's geometry depends on it
     with _PLANS_LOCK:
         plan = _PLANS.get(key)
         if plan is None:

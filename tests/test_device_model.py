@@ -40,8 +40,8 @@ def decode_A(a_img, e_words):
 
 def tile_model(plan, dense, halo):
     kern = plan.kernel
-    r = kern.r
     inf = plan.info()
+    r = inf.r_dev or kern.r  # device radius: a radius-2 stencil runs embedded as radius 3
     L, n_tile = inf.L, inf.n_tile * (2 if inf.cg2 else 1)  # a CTA pair spans both x-halves
     a_img, e_words, starts = plan.operands()
     in_off, out_off = plan.geometry()
@@ -186,3 +186,21 @@ def test_lane_map_is_a_permutation():
                     assert lanes[inf.L * a + i] in (pair, inf.L * a + i)
                 else:
                     assert lanes[inf.L * a + i] == inf.L * a + i
+
+
+def test_radius2_embeds_as_radius3():
+    """1D / 2D radius 2 runs on the L = 8 fast path (zero ring); SPD_NO_EMBED
+    keeps the generic L = 6 geometry."""
+    import os
+
+    for d in (1, 2):
+        c = np.ones((5,) * d)
+        kern = sp.make_kernel("box", d, 2, c)
+        inf = Plan(kern, "even", "fp16", device=-1).info()
+        assert inf.L == 8 and inf.r_dev == 3
+        os.environ["SPD_NO_EMBED"] = "1"
+        try:
+            inf = Plan(kern, "even", "fp16", device=-1).info()
+        finally:
+            del os.environ["SPD_NO_EMBED"]
+        assert inf.L == 6 and inf.r_dev == 2

@@ -376,18 +376,24 @@ def test_persistent_launch_matches_per_step(monkeypatch, d, r, shape, steps, swe
         (2, 1, (1000, 4096), 3),     # B9 geometry, ragged last tile row
         (2, 1, (2048, 2000), 2),     # ragged right tiles
         (2, 3, (1000, 4096), 2),     # B49 geometry
-        (2, 2, (600, 3072), 2),      # generic L = 6
+        (2, 2, (600, 3072), 2),      # radius 2 embedded as radius 3 (L = 8 fast path)
+        (2, 2, (600, 3066), 2),      # ... with a partial last 8-point chunk (width % 8 = 2)
+        ("noembed", 2, (600, 3072), 2),  # radius 2 on the generic L = 6 path (SPD_NO_EMBED)
         (2, 4, (300, 4000), 1),      # generic L = 10
         (2, 7, (200, 4096), 1),      # generic L = 16
         (3, 1, (60, 72, 512), 2),    # B27 geometry, ragged z / y
         (1, 1, (1, 4 * 512 * 700), 2),
+        (1, 2, (1, 419994), 2),      # 1D radius 2 embedded, partial last chunk
     ],
 )
 @pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.timeout(180, method="thread")
-def test_many_tiles_per_cta_match_oracle(d, r, shape, steps, persistent):
+def test_many_tiles_per_cta_match_oracle(monkeypatch, d, r, shape, steps, persistent):
     import os
 
+    if d == "noembed":
+        monkeypatch.setenv("SPD_NO_EMBED", "1")
+        d = 2
     rng = np.random.default_rng([d, r, 11])
     c = rng.uniform(0.5, 1.5, (2 * r + 1,) * d)
     c /= c.sum()
