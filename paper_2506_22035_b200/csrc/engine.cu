@@ -366,6 +366,9 @@ struct StepParams {
 // Epilogue: kEpiGroups groups of 4 warps (one warp per TMEM lane quadrant);
 // group g drains the accumulators of the tiles it == g (mod kEpiGroups), so
 // the TMEM -> register -> global path of consecutive tiles overlaps.
+#ifndef SPD_3D_NSTAGE
+#define SPD_3D_NSTAGE 2
+#endif
 #ifndef SPD_3D_NNAT
 #define SPD_3D_NNAT 4  // 3D natural-row stages (tools/build_variant.sh scans)
 #endif
@@ -414,6 +417,15 @@ struct StepParams {
 #endif
 #ifndef SPD_L8_ITEMGROUP
 #define SPD_L8_ITEMGROUP 0
+#endif
+#ifndef SPD_L8_NSTAGE
+#define SPD_L8_NSTAGE 3
+#endif
+#ifndef SPD_L8_NNAT
+#define SPD_L8_NNAT 4
+#endif
+#ifndef SPD_L8_NACC
+#define SPD_L8_NACC 4
 #endif
 #ifndef SPD_GEN_PW
 #define SPD_GEN_PW 8
@@ -1939,11 +1951,13 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
     return launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, SPD_2D_NACC, 34>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
-    return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40, false, SPD_3D_PW>(plan, sp, st);
+    return launch_step<T, 4, PARITY, 32, SPD_3D_NSTAGE, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40, false, SPD_3D_PW>(plan,
+                                                                                                              sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.cg2)
     return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, 3, 100, 1, 0, true, SPD_3D_PW>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 22)
-    return launch_step<T, 8, PARITY, 64, 3, 4, 4, 22, 1, 0, false, SPD_L8_PW>(plan, sp, st);
+    return launch_step<T, 8, PARITY, 64, SPD_L8_NSTAGE, SPD_L8_NNAT, SPD_L8_NACC, 22, 1, 0, false, SPD_L8_PW>(plan, sp,
+                                                                                                            st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 16)
     return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16, 1, 0, false, SPD_L8_PW>(plan, sp, st);
   // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
