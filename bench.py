@@ -363,7 +363,14 @@ def measure(ctx: Ctx, args, cfg_name: str, exchange: str) -> dict:
             # one host call and one launch per timestep, no NCCL on the data path
             try:
                 peer = PeerSlab(plan, slab, ops.grid, compute_stream=stream, comm_stream=comm)
-                launches_per_step = T
+                # spd_slab_step: one edge-first launch per timestep for small 2D slabs,
+                # an edge launch + an interior launch for 3D and large slabs (csrc/peer.cu)
+                tiles = -(-shape[-1] // (info.n_tile * info.L)) * -(-shape[-2 if d >= 2 else -1] // info.tile_y)
+                if d == 3:
+                    tiles *= -(-shape[0] // info.tile_z)
+                env = os.environ.get("SPD_SLAB_TWO_LAUNCH")
+                two = bool(int(env)) if env else (d == 3 or tiles >= 10000)
+                launches_per_step = T * (2 if two else 1)
             except Exception as exc:  # IPC / peer access unavailable: NCCL send/recv driver (all ranks)
                 print(f"peer exchange unavailable ({exc}); using NCCL send/recv", file=sys.stderr)
                 exchange = "nccl"
