@@ -358,6 +358,12 @@ struct StepParams {
   int reverse;               // step 0 traverses tiles last-to-first; steps alternate
   int dbg;                   // development switches (SPD_DBG; read only in -DSPD_DEVEL builds)
   int item_fence;            // always 0: a uniform branch per 2D r = 1 producer item (see the producer)
+  // Slab step with fused peer stores: output rows (2D) / planes (3D) u < peer_rows are also
+  // stored into peer_out[0] at row u + peer_row[0] (the up neighbour's bottom halo), rows
+  // u >= row_hi - peer_rows into peer_out[1] at u + peer_row[1] (the down neighbour's top halo)
+  void* peer_out[2];
+  int64_t peer_row[2];
+  int peer_rows;
   unsigned long long* trace; // debug timeline (CTA 0): [event][tile] globaltimer stamps, or null
   const uint16_t* a_img;     // [S][128][16] compressed values (fp16/bf16 bits)
   const uint32_t* e_words;   // [S][128]
@@ -763,6 +769,17 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     return id;
   };
 
+
+  // Fused peer stores (slab step): the neighbours' copies of output row
+  // (2D) / plane (3D) u, whose element offset in this grid is `off`.
+  auto peer_rows_of = [&](int64_t off, int64_t u, T* (&pr)[2]) {
+    pr[0] = pr[1] = nullptr;
+    if (p.peer_rows == 0) return;
+    const int64_t unit = g.d == 3 ? p.plane : p.pitch;
+    if (p.peer_out[0] && u < p.peer_rows) pr[0] = static_cast<T*>(p.peer_out[0]) + off + p.peer_row[0] * unit;
+    if (p.peer_out[1] && u >= p.row_hi - p.peer_rows)
+      pr[1] = static_cast<T*>(p.peer_out[1]) + off + p.peer_row[1] * unit;
+  };
 
   // Publisher (persistent launches): after all epilogue warps issued a
   // tile's stores (pubf), make them visible at gpu scope and bump the tile's
@@ -1397,6 +1414,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       bool row_ok[MT][2];
       int64_t chunk_lim[MT][2];  // valid chunks in this row
       T* orow[MT][2];
+      T* prow[MT][2][2];  // fused peer stores of this row (up, down neighbour), or null
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -1409,6 +1427,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           else row_ok[mt][h] = true;
           chunk_lim[mt][h] = (p.nx - xr) / L;
           orow[mt][h] = out + p.origin + z * p.plane + y * p.pitch + xr;
+          peer_rows_of(orow[mt][h] - out, g.d == 3 ? z : y, prow[mt][h]);
         }
       if (warp == 0 && lane == 0) SPD_TRACE(12, it);
       mbar_wait(bar_accf + 8 * acc, aphase);
@@ -1443,14 +1462,20 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           }
           if (!row_ok[mt][h] || SPD_DBG_BIT(1)) continue;
           const int64_t ch0 = (int64_t)cb * 32 + (hi ? 16 : 0) + 4 * cq;
-          T* dst = orow[mt][h] + ch0 * L;
-          if (ch0 + 4 <= chunk_lim[mt][h]) {
-            stg_v8(dst, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
-          } else {
+          auto put = [&](T* rowp) {
+            T* dst = rowp + ch0 * L;
+            if (ch0 + 4 <= chunk_lim[mt][h]) {
+              stg_v8(dst, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+            } else {
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-              if (ch0 + c < chunk_lim[mt][h]) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(o[2 * c], o[2 * c + 1]);
-          }
+              for (int c = 0; c < 4; ++c)
+                if (ch0 + c < chunk_lim[mt][h])
+                  *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(o[2 * c], o[2 * c + 1]);
+            }
+          };
+          put(orow[mt][h]);
+          if (prow[mt][h][0]) put(prow[mt][h][0]);
+          if (prow[mt][h][1]) put(prow[mt][h][1]);
         }
       };
       uint32_t va[2][16], vb[2][16];
@@ -1516,6 +1541,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       int64_t x_lim[MT];      // valid points of this row from its chunk 0 (a partial last chunk:
                               // an embedded radius-2 grid's width is a multiple of 6, not 8)
       T* orow[MT];
+      T* prow[MT][2];         // fused peer stores of this row (up, down neighbour), or null
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int64_t z = id.z0 + odz[mt];
@@ -1527,6 +1553,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
         x_lim[mt] = p.nx - xr;
         chunk_lim[mt] = x_lim[mt] / L;
         orow[mt] = out + p.origin + z * p.plane + y * p.pitch + xr;
+        peer_rows_of(orow[mt] - out, g.d == 3 ? z : y, prow[mt]);
       }
       if (warp == 0 && lane == 0) SPD_TRACE(12, it);
       mbar_wait(bar_accf + 8 * acc, aphase);
@@ -1578,27 +1605,32 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
               w[(2 * k + h) * (L / 2) + u] =
                   __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
         const int64_t c_lane = (int64_t)cb * 32 + PPD * d;  // first chunk of piece 0; piece 1 at +16
-        T* dst = orow[mt] + c_lane * L;
-        if (c_lane + 16 + PPD <= chunk_lim[mt]) {
-          stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
-          stg_v8(dst + 16 * L, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
-        } else {
+        auto put = [&](T* rowp) {
+          T* dst = rowp + c_lane * L;
+          if (c_lane + 16 + PPD <= chunk_lim[mt]) {
+            stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+            stg_v8(dst + 16 * L, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+          } else {
 #pragma unroll
-          for (int c = 0; c < 2 * PPD; ++c) {
-            const int64_t ch = c_lane + (c / PPD) * 16 + c % PPD;
-            if (ch < chunk_lim[mt]) {
-              T* dc = orow[mt] + ch * L;
-              if (L == 4) *reinterpret_cast<uint2*>(dc) = make_uint2(w[2 * c], w[2 * c + 1]);
-              else *reinterpret_cast<uint4*>(dc) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-            } else if (ch * L < x_lim[mt]) {  // partial last chunk: point by point
-              uint16_t* dc = reinterpret_cast<uint16_t*>(orow[mt] + ch * L);
-              const int n = (int)(x_lim[mt] - ch * L);
+            for (int c = 0; c < 2 * PPD; ++c) {
+              const int64_t ch = c_lane + (c / PPD) * 16 + c % PPD;
+              if (ch < chunk_lim[mt]) {
+                T* dc = rowp + ch * L;
+                if (L == 4) *reinterpret_cast<uint2*>(dc) = make_uint2(w[2 * c], w[2 * c + 1]);
+                else *reinterpret_cast<uint4*>(dc) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+              } else if (ch * L < x_lim[mt]) {  // partial last chunk: point by point
+                uint16_t* dc = reinterpret_cast<uint16_t*>(rowp + ch * L);
+                const int n = (int)(x_lim[mt] - ch * L);
 #pragma unroll
-              for (int e = 0; e < L; ++e)
-                if (e < n) dc[e] = (uint16_t)(w[(L / 2) * c + e / 2] >> (16 * (e & 1)));
+                for (int e = 0; e < L; ++e)
+                  if (e < n) dc[e] = (uint16_t)(w[(L / 2) * c + e / 2] >> (16 * (e & 1)));
+              }
             }
           }
-        }
+        };
+        put(orow[mt]);
+        if (prow[mt][0]) put(prow[mt][0]);
+        if (prow[mt][1]) put(prow[mt][1]);
       };
       uint32_t va[32], vb[32];
       uint32_t b0[16], b1[16];
@@ -2431,7 +2463,26 @@ int spd_step_range(const spd_plan* plan, const spd_grid_desc* gd, const void* in
 }
 
 int spd_step_edges(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, void* stream) {
-  using namespace spd;
+  return spd::step_edges_ex(plan, gd, in, out, nullptr, stream);
+}
+
+}  // extern "C"
+
+namespace spd {
+
+static void set_peer_stores(StepParams& sp, const PeerStores* ps) {
+  if (!ps) return;
+  sp.peer_out[0] = ps->out[0];
+  sp.peer_out[1] = ps->out[1];
+  sp.peer_row[0] = ps->row[0];
+  sp.peer_row[1] = ps->row[1];
+  sp.peer_rows = ps->rows;
+}
+
+bool plan_peer_stores(const spd_plan* plan) { return plan && !plan->g.cg2 && (plan->g.L == 4 || plan->g.L == 8); }
+
+int step_edges_ex(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, const PeerStores* ps,
+                  void* stream) {
   int rc = check_desc(plan, gd);
   if (rc) return rc;
   if (plan->d == 1) return set_error(SPD_EINVAL, "edge bands are defined for 2D / 3D grids");
@@ -2446,8 +2497,34 @@ int spd_step_edges(const spd_plan* plan, const spd_grid_desc* gd, const void* in
     sp.n_tiles = sp.tiles_x * sp.tiles_y * sp.tiles_z;
     sp.n_bands = 2;
   }
+  if (ps && !plan_peer_stores(plan)) return set_error(SPD_EUNSUPPORTED, "no fused peer stores for this geometry");
+  set_peer_stores(sp, ps);
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
+
+int step_edge_first_ex(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int dir,
+                       unsigned int* band_done, int publish, const PeerStores* ps, void* stream) {
+  int rc = check_desc(plan, gd);
+  if (rc) return rc;
+  if (plan->d == 1) return set_error(SPD_EINVAL, "band orders are defined for 2D / 3D grids");
+  if (plan->g.cg2) return set_error(SPD_EUNSUPPORTED, "edge-first launch not supported in CTA-pair mode");
+  if (dir != 0 && dir != 1) return set_error(SPD_EINVAL, "interior direction must be 0 or 1, got %d", dir);
+  if (publish && !band_done) return set_error(SPD_EINVAL, "publishing needs band counters");
+  if (ps && !plan_peer_stores(plan)) return set_error(SPD_EUNSUPPORTED, "no fused peer stores for this geometry");
+  const int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
+  StepParams sp;
+  rc = fill_step_params(plan, gd, in, out, 0, extent, 1, sp);
+  if (rc) return rc;
+  sp.edge_order = dir + 1;
+  sp.publish = publish ? 1 : 0;
+  sp.band_done = band_done;
+  set_peer_stores(sp, ps);
+  return dispatch(plan, sp, (cudaStream_t)stream);
+}
+
+}  // namespace spd
+
+extern "C" {
 
 int spd_step_ordered(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, const void* order,
                      int n_pairs, unsigned int* band_done, int publish, void* stream) {
@@ -2472,21 +2549,7 @@ int spd_step_ordered(const spd_plan* plan, const spd_grid_desc* gd, const void* 
 
 int spd_step_edge_first(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, int dir,
                         unsigned int* band_done, int publish, void* stream) {
-  using namespace spd;
-  int rc = check_desc(plan, gd);
-  if (rc) return rc;
-  if (plan->d == 1) return set_error(SPD_EINVAL, "band orders are defined for 2D / 3D grids");
-  if (plan->g.cg2) return set_error(SPD_EUNSUPPORTED, "edge-first launch not supported in CTA-pair mode");
-  if (dir != 0 && dir != 1) return set_error(SPD_EINVAL, "interior direction must be 0 or 1, got %d", dir);
-  if (publish && !band_done) return set_error(SPD_EINVAL, "publishing needs band counters");
-  const int64_t extent = plan->d == 3 ? gd->nz : gd->ny;
-  StepParams sp;
-  rc = fill_step_params(plan, gd, in, out, 0, extent, 1, sp);
-  if (rc) return rc;
-  sp.edge_order = dir + 1;
-  sp.publish = publish ? 1 : 0;
-  sp.band_done = band_done;
-  return dispatch(plan, sp, (cudaStream_t)stream);
+  return spd::step_edge_first_ex(plan, gd, in, out, dir, band_done, publish, nullptr, stream);
 }
 
 int spd_run(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* buf1, int steps, void* stream) {

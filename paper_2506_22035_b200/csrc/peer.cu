@@ -234,8 +234,20 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
   static const char* two_env = getenv("SPD_SLAB_TWO_LAUNCH");
   const bool two_launch = two_env ? atoi(two_env) != 0
                                   : (s->g.dims == 3 || (int64_t)s->per_band * s->n_bands >= 10000);
+  // Fused peer stores: the edge tiles' epilogue writes the r outermost rows
+  // straight into the neighbours' halo rows (NVLink stores; same layout), so
+  // the comm stream only signals -- no copy.  Geometries without them (the
+  // generic radii) keep the copy-engine exchange.  SPD_SLAB_COPY=1 forces it.
+  static const char* copy_env = getenv("SPD_SLAB_COPY");
+  const bool fused = plan_peer_stores(s->plan) && !(copy_env && atoi(copy_env) != 0);
+  PeerStores ps;
+  ps.out[0] = s->has_up ? s->up_buf[(t + 1) & 1] : nullptr;
+  ps.out[1] = s->has_dn ? s->dn_buf[(t + 1) & 1] : nullptr;
+  ps.row[0] = s->up_extent;  // my row u -> the up neighbour's row up_extent + u (its bottom halo)
+  ps.row[1] = -s->extent;    // my row u -> the down neighbour's row u - extent (its top halo)
+  ps.rows = s->r;
   if ((s->has_up || s->has_dn) && !two_launch) {
-    int rc0 = spd_step_edge_first(s->plan, &s->g, in, out, t & 1, s->band_done, 1, cs);
+    int rc0 = step_edge_first_ex(s->plan, &s->g, in, out, t & 1, s->band_done, 1, fused ? &ps : nullptr, cs);
     if (rc0) return rc0;
     const cuuint32_t target = (cuuint32_t)((int64_t)(t + 1) * s->per_band);
     const size_t bytes = (size_t)s->r * s->unit * 2;
@@ -245,8 +257,9 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
                       "wait top band");
       if (rc) return rc;
       uint16_t* dst = (uint16_t*)s->up_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, s->up_extent);
-      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, 0), bytes, cudaMemcpyDeviceToDevice, xs),
-                  "peer copy up");
+      if (!fused)
+        rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, 0), bytes, cudaMemcpyDeviceToDevice, xs),
+                    "peer copy up");
       if (rc) return rc;
       rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->up_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
                   "signal up");
@@ -257,9 +270,10 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
                       "wait bottom band");
       if (rc) return rc;
       uint16_t* dst = (uint16_t*)s->dn_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, -s->r);
-      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, s->extent - s->r), bytes,
-                                  cudaMemcpyDeviceToDevice, xs),
-                  "peer copy down");
+      if (!fused)
+        rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, s->extent - s->r), bytes,
+                                    cudaMemcpyDeviceToDevice, xs),
+                    "peer copy down");
       if (rc) return rc;
       rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->dn_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
                   "signal down");
@@ -270,7 +284,9 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
   // 2b. boundary bands (one launch), then the exchange on the comm stream
   const int64_t last = ((s->extent - 1) / s->band) * s->band;
   const bool split = last > s->band;
-  int rc = split ? spd_step_edges(s->plan, &s->g, in, out, cs) : spd_step_range(s->plan, &s->g, in, out, 0, s->extent, cs);
+  int rc = split ? step_edges_ex(s->plan, &s->g, in, out, fused ? &ps : nullptr, cs)
+                 : (fused ? step_edge_first_ex(s->plan, &s->g, in, out, t & 1, nullptr, 0, &ps, cs)
+                          : spd_step_range(s->plan, &s->g, in, out, 0, s->extent, cs));
   if (rc) return rc;
   if (s->has_up || s->has_dn) {
     rc = rt_err(cudaEventRecord(s->boundary_done, cs), "event record");
@@ -281,8 +297,9 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
     const uint16_t* o = (const uint16_t*)out;
     if (s->has_up) {  // my first r rows -> up neighbour's bottom halo (rows extent_up ..)
       uint16_t* dst = (uint16_t*)s->up_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, s->up_extent);
-      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, 0), bytes, cudaMemcpyDeviceToDevice, xs),
-                  "peer copy up");
+      if (!fused)
+        rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, 0), bytes, cudaMemcpyDeviceToDevice, xs),
+                    "peer copy up");
       if (rc) return rc;
       rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->up_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
                   "signal up");
@@ -290,9 +307,10 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
     }
     if (s->has_dn) {  // my last r rows -> down neighbour's top halo (rows -r ..)
       uint16_t* dst = (uint16_t*)s->dn_buf[(t + 1) & 1] + unit_start(&s->g, s->unit, -s->r);
-      rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, s->extent - s->r), bytes,
-                                  cudaMemcpyDeviceToDevice, xs),
-                  "peer copy down");
+      if (!fused)
+        rc = rt_err(cudaMemcpyAsync(dst, o + unit_start(&s->g, s->unit, s->extent - s->r), bytes,
+                                    cudaMemcpyDeviceToDevice, xs),
+                    "peer copy down");
       if (rc) return rc;
       rc = cu_err(f.write((CUstream)xs, (CUdeviceptr)s->dn_flag, (cuuint32_t)(t + 1), CU_STREAM_WRITE_VALUE_DEFAULT),
                   "signal down");

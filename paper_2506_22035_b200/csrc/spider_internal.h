@@ -57,6 +57,20 @@ struct Geometry {
   int out_dz[SPD_MAX_ROUT], out_dy[SPD_MAX_ROUT], out_dx[SPD_MAX_ROUT];
 };
 
+// Fused peer stores of a slab step (peer.cu): output rows (2D) / planes (3D)
+// u < rows also go to out[0] at u + row[0], rows u >= extent - rows to
+// out[1] at u + row[1] (the neighbours' halo rows, same layout).
+struct PeerStores {
+  void* out[2];
+  int64_t row[2];
+  int rows;
+};
+bool plan_peer_stores(const spd_plan* plan);  // the plan's epilogue supports them
+int step_edge_first_ex(const spd_plan* plan, const spd_grid_desc* g, const void* in, void* out, int dir,
+                       unsigned int* band_done, int publish, const PeerStores* ps, void* stream);
+int step_edges_ex(const spd_plan* plan, const spd_grid_desc* g, const void* in, void* out, const PeerStores* ps,
+                  void* stream);
+
 int build_geometry(int d, int r, int flags, Geometry* g);
 int lane_of(const Geometry& g, int a, int i);
 int pack_operands(const Geometry& g, int n_rows, const double* row_values,
