@@ -770,17 +770,6 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
   };
 
 
-  // Fused peer stores (slab step): the neighbours' copies of output row
-  // (2D) / plane (3D) u, whose element offset in this grid is `off`.
-  auto peer_rows_of = [&](int64_t off, int64_t u, T* (&pr)[2]) {
-    pr[0] = pr[1] = nullptr;
-    if (p.peer_rows == 0) return;
-    const int64_t unit = g.d == 3 ? p.plane : p.pitch;
-    if (p.peer_out[0] && u < p.peer_rows) pr[0] = static_cast<T*>(p.peer_out[0]) + off + p.peer_row[0] * unit;
-    if (p.peer_out[1] && u >= p.row_hi - p.peer_rows)
-      pr[1] = static_cast<T*>(p.peer_out[1]) + off + p.peer_row[1] * unit;
-  };
-
   // Publisher (persistent launches): after all epilogue warps issued a
   // tile's stores (pubf), make them visible at gpu scope and bump the tile's
   // band counter.  Tiles whose stores are already issued are batched behind
@@ -792,16 +781,56 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
   auto pub_tile = [&](const TileId& id) {
     return p.steps > 1 || p.chain || id.band == 0 || id.band == p.n_bands - 1;
   };
+  // Slab step, fused peer stores: once an edge tile's outputs are stored, the
+  // publisher warp copies its rows (2D) / planes (3D) u < peer_rows into the
+  // up neighbour's halo (row u + peer_row[0]) and u >= row_hi - peer_rows into
+  // the down neighbour's (u + peer_row[1]) -- peer-memory stores from inside
+  // the step kernel, tile by tile, while the interior is still computing.
+  // Only interior x is copied: the neighbours' x-halo columns are Dirichlet
+  // constants.  16-byte vectors (x = 0 is 32-byte aligned), scalar tail.
+  auto peer_copy = [&](const TileId& id) {
+    const T* src_base = static_cast<const T*>(p.buf[(id.step + 1) & 1]);
+    const int64_t unit = g.d == 3 ? p.plane : p.pitch;
+    const int64_t xw = min((int64_t)g.tile_x, p.nx - id.x0);  // points of this tile's rows
+    const int64_t nvec = xw / 8;
+    const int rows_y = g.d == 3 ? (int)min((int64_t)g.tile_y, p.ny - id.y0) : 1;
+    const int64_t u0 = g.d == 3 ? id.z0 : id.y0;
+    const int nu = g.d == 3 ? g.tile_z : g.tile_y;
+    for (int k = 0; k < 2; ++k) {
+      if (!p.peer_out[k]) continue;
+      T* dst_base = static_cast<T*>(p.peer_out[k]);
+      for (int du = 0; du < nu; ++du) {
+        const int64_t u = u0 + du;
+        if (u >= p.row_hi) break;
+        if (k == 0 ? u >= p.peer_rows : u < p.row_hi - p.peer_rows) continue;
+        for (int ry = 0; ry < rows_y; ++ry) {
+          const int64_t off = p.origin + (g.d == 3 ? u * p.plane + (id.y0 + ry) * p.pitch : u * p.pitch) + id.x0;
+          const T* src = src_base + off;
+          T* dst = dst_base + off + p.peer_row[k] * unit;
+          for (int64_t v = lane; v < nvec; v += 32)
+            reinterpret_cast<uint4*>(dst)[v] = __ldcg(reinterpret_cast<const uint4*>(src) + v);
+          for (int64_t e = nvec * 8 + lane; e < xw; e += 32)
+            reinterpret_cast<uint16_t*>(dst)[e] = __ldcg(reinterpret_cast<const unsigned short*>(src) + e);
+        }
+      }
+    }
+  };
   auto publisher = [&]() {
-    if (p.steps == 1 && !p.chain) {
+    if (p.steps == 1 && !p.chain) {  // the whole warp runs this form
       int pit = 0;
       for (int gi = wid0; gi < total; gi += wstride) {
         const TileId id = decode_e(gi, fetch(gi));
         if (!pub_tile(id)) continue;
-        mbar_wait_sleep(bar_pubf + 8 * (pit % kNPub), (pit / kNPub) & 1);
-        asm volatile("fence.acq_rel.sys;" ::: "memory");  // observed by a copy engine
-        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
-        mbar_arrive(bar_pube + 8 * (pit % kNPub));
+        mbar_wait_sleep(bar_pubf + 8 * (pit % kNPub), (pit / kNPub) & 1);  // every lane acquires
+        if (p.peer_rows) peer_copy(id);
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.acq_rel.sys;" ::: "memory");  // observed by the neighbour / a copy engine
+          if (p.band_done)
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(p.band_done + id.band) : "memory");
+          mbar_arrive(bar_pube + 8 * (pit % kNPub));
+        }
+        __syncwarp();
         ++pit;
       }
       return;
@@ -1098,7 +1127,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     }
     }
   } else if (warp == kPubWarp) {
-    if (publishing && lane == 0 && !SPD_DBG_BIT(2048)) publisher();
+    if (publishing && (lane == 0 || (p.steps == 1 && !p.chain)) && !SPD_DBG_BIT(2048)) publisher();
   } else if (warp == kPollWarp) {
     // ===================== dependency poller (persistent launches) =========
     // Tiles whose dependencies are already met are released in batches of
@@ -1414,7 +1443,6 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       bool row_ok[MT][2];
       int64_t chunk_lim[MT][2];  // valid chunks in this row
       T* orow[MT][2];
-      T* prow[MT][2][2];  // fused peer stores of this row (up, down neighbour), or null
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -1427,7 +1455,6 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           else row_ok[mt][h] = true;
           chunk_lim[mt][h] = (p.nx - xr) / L;
           orow[mt][h] = out + p.origin + z * p.plane + y * p.pitch + xr;
-          peer_rows_of(orow[mt][h] - out, g.d == 3 ? z : y, prow[mt][h]);
         }
       if (warp == 0 && lane == 0) SPD_TRACE(12, it);
       mbar_wait(bar_accf + 8 * acc, aphase);
@@ -1462,20 +1489,14 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           }
           if (!row_ok[mt][h] || SPD_DBG_BIT(1)) continue;
           const int64_t ch0 = (int64_t)cb * 32 + (hi ? 16 : 0) + 4 * cq;
-          auto put = [&](T* rowp) {
-            T* dst = rowp + ch0 * L;
-            if (ch0 + 4 <= chunk_lim[mt][h]) {
-              stg_v8(dst, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
-            } else {
+          T* dst = orow[mt][h] + ch0 * L;
+          if (ch0 + 4 <= chunk_lim[mt][h]) {
+            stg_v8(dst, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+          } else {
 #pragma unroll
-              for (int c = 0; c < 4; ++c)
-                if (ch0 + c < chunk_lim[mt][h])
-                  *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(o[2 * c], o[2 * c + 1]);
-            }
-          };
-          put(orow[mt][h]);
-          if (prow[mt][h][0]) put(prow[mt][h][0]);
-          if (prow[mt][h][1]) put(prow[mt][h][1]);
+            for (int c = 0; c < 4; ++c)
+              if (ch0 + c < chunk_lim[mt][h]) *reinterpret_cast<uint2*>(dst + c * L) = make_uint2(o[2 * c], o[2 * c + 1]);
+          }
         }
       };
       uint32_t va[2][16], vb[2][16];
@@ -1541,7 +1562,6 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
       int64_t x_lim[MT];      // valid points of this row from its chunk 0 (a partial last chunk:
                               // an embedded radius-2 grid's width is a multiple of 6, not 8)
       T* orow[MT];
-      T* prow[MT][2];         // fused peer stores of this row (up, down neighbour), or null
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
         const int64_t z = id.z0 + odz[mt];
@@ -1553,7 +1573,6 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
         x_lim[mt] = p.nx - xr;
         chunk_lim[mt] = x_lim[mt] / L;
         orow[mt] = out + p.origin + z * p.plane + y * p.pitch + xr;
-        peer_rows_of(orow[mt] - out, g.d == 3 ? z : y, prow[mt]);
       }
       if (warp == 0 && lane == 0) SPD_TRACE(12, it);
       mbar_wait(bar_accf + 8 * acc, aphase);
@@ -1605,32 +1624,27 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
               w[(2 * k + h) * (L / 2) + u] =
                   __byte_perm(bw[k * L + 2 * u], bw[k * L + 2 * u + 1], h ? 0x7632 : 0x5410);
         const int64_t c_lane = (int64_t)cb * 32 + PPD * d;  // first chunk of piece 0; piece 1 at +16
-        auto put = [&](T* rowp) {
-          T* dst = rowp + c_lane * L;
-          if (c_lane + 16 + PPD <= chunk_lim[mt]) {
-            stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
-            stg_v8(dst + 16 * L, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
-          } else {
+        T* dst = orow[mt] + c_lane * L;
+        if (c_lane + 16 + PPD <= chunk_lim[mt]) {
+          stg_v8(dst, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+          stg_v8(dst + 16 * L, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+        } else {
 #pragma unroll
-            for (int c = 0; c < 2 * PPD; ++c) {
-              const int64_t ch = c_lane + (c / PPD) * 16 + c % PPD;
-              if (ch < chunk_lim[mt]) {
-                T* dc = rowp + ch * L;
-                if (L == 4) *reinterpret_cast<uint2*>(dc) = make_uint2(w[2 * c], w[2 * c + 1]);
-                else *reinterpret_cast<uint4*>(dc) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
-              } else if (ch * L < x_lim[mt]) {  // partial last chunk: point by point
-                uint16_t* dc = reinterpret_cast<uint16_t*>(rowp + ch * L);
-                const int n = (int)(x_lim[mt] - ch * L);
+          for (int c = 0; c < 2 * PPD; ++c) {
+            const int64_t ch = c_lane + (c / PPD) * 16 + c % PPD;
+            if (ch < chunk_lim[mt]) {
+              T* dc = orow[mt] + ch * L;
+              if (L == 4) *reinterpret_cast<uint2*>(dc) = make_uint2(w[2 * c], w[2 * c + 1]);
+              else *reinterpret_cast<uint4*>(dc) = make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+            } else if (ch * L < x_lim[mt]) {  // partial last chunk: point by point
+              uint16_t* dc = reinterpret_cast<uint16_t*>(orow[mt] + ch * L);
+              const int n = (int)(x_lim[mt] - ch * L);
 #pragma unroll
-                for (int e = 0; e < L; ++e)
-                  if (e < n) dc[e] = (uint16_t)(w[(L / 2) * c + e / 2] >> (16 * (e & 1)));
-              }
+              for (int e = 0; e < L; ++e)
+                if (e < n) dc[e] = (uint16_t)(w[(L / 2) * c + e / 2] >> (16 * (e & 1)));
             }
           }
-        };
-        put(orow[mt]);
-        if (prow[mt][0]) put(prow[mt][0]);
-        if (prow[mt][1]) put(prow[mt][1]);
+        }
       };
       uint32_t va[32], vb[32];
       uint32_t b0[16], b1[16];
@@ -2479,7 +2493,7 @@ static void set_peer_stores(StepParams& sp, const PeerStores* ps) {
   sp.peer_rows = ps->rows;
 }
 
-bool plan_peer_stores(const spd_plan* plan) { return plan && !plan->g.cg2 && (plan->g.L == 4 || plan->g.L == 8); }
+bool plan_peer_stores(const spd_plan* plan) { return plan && !plan->g.cg2; }
 
 int step_edges_ex(const spd_plan* plan, const spd_grid_desc* gd, const void* in, void* out, const PeerStores* ps,
                   void* stream) {
@@ -2499,6 +2513,7 @@ int step_edges_ex(const spd_plan* plan, const spd_grid_desc* gd, const void* in,
   }
   if (ps && !plan_peer_stores(plan)) return set_error(SPD_EUNSUPPORTED, "no fused peer stores for this geometry");
   set_peer_stores(sp, ps);
+  if (ps) sp.publish = 1;  // the publisher warp makes the peer stores (no band counters)
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
 
@@ -2516,8 +2531,8 @@ int step_edge_first_ex(const spd_plan* plan, const spd_grid_desc* gd, const void
   rc = fill_step_params(plan, gd, in, out, 0, extent, 1, sp);
   if (rc) return rc;
   sp.edge_order = dir + 1;
-  sp.publish = publish ? 1 : 0;
-  sp.band_done = band_done;
+  sp.publish = (publish || ps) ? 1 : 0;
+  sp.band_done = publish ? band_done : nullptr;
   set_peer_stores(sp, ps);
   return dispatch(plan, sp, (cudaStream_t)stream);
 }
