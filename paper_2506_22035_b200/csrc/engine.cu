@@ -581,6 +581,51 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
+// Slab step, fused peer stores (called by the publisher warp, all lanes): the
+// tile at (z0, y0, x0)'s rows (2D) / planes (3D) u < peer_rows go to the up
+// neighbour's halo (row u + peer_row[0]), u >= row_hi - peer_rows to the down
+// neighbour's (u + peer_row[1]).  Only interior x is copied: the neighbours'
+// x-halo columns are Dirichlet constants.  16-byte vectors (x = 0 is 32-byte
+// aligned), scalar tail.  Inlined or called out of line per geometry: the
+// choice moves the whole kernel's code layout, and the two geometries that
+// react prefer opposite ones (B27 inlined 123 vs 130 us, B49 out of line 100
+// vs 103; profiles/r02_slab_step.txt).
+template <typename T>
+__device__ __forceinline__ void peer_copy_tile(const StepParams& p, const T* src_base, int64_t z0, int64_t y0,
+                                               int64_t x0, int lane) {
+  const Geometry& g = p.g;
+  const int64_t unit = g.d == 3 ? p.plane : p.pitch;
+  const int64_t xw = min((int64_t)g.tile_x, p.nx - x0);
+  const int64_t nvec = xw / 8;
+  const int rows_y = g.d == 3 ? (int)min((int64_t)g.tile_y, p.ny - y0) : 1;
+  const int64_t u0 = g.d == 3 ? z0 : y0;
+  const int nu = g.d == 3 ? g.tile_z : g.tile_y;
+  for (int k = 0; k < 2; ++k) {
+    if (!p.peer_out[k]) continue;
+    T* dst_base = static_cast<T*>(p.peer_out[k]);
+    for (int du = 0; du < nu; ++du) {
+      const int64_t u = u0 + du;
+      if (u >= p.row_hi) break;
+      if (k == 0 ? u >= p.peer_rows : u < p.row_hi - p.peer_rows) continue;
+      for (int ry = 0; ry < rows_y; ++ry) {
+        const int64_t off = p.origin + (g.d == 3 ? u * p.plane + (y0 + ry) * p.pitch : u * p.pitch) + x0;
+        const T* src = src_base + off;
+        T* dst = dst_base + off + p.peer_row[k] * unit;
+        for (int64_t v = lane; v < nvec; v += 32)
+          reinterpret_cast<uint4*>(dst)[v] = __ldcg(reinterpret_cast<const uint4*>(src) + v);
+        for (int64_t e = nvec * 8 + lane; e < xw; e += 32)
+          reinterpret_cast<uint16_t*>(dst)[e] = __ldcg(reinterpret_cast<const unsigned short*>(src) + e);
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ __noinline__ void peer_copy_tile_call(const StepParams& p, const T* src_base, int64_t z0, int64_t y0,
+                                                 int64_t x0, int lane) {
+  peer_copy_tile<T>(p, src_base, z0, y0, x0, lane);
+}
+
 // ---------------------------------------------------------------------------
 // The stencil step kernel.
 //
@@ -782,38 +827,13 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     return p.steps > 1 || p.chain || id.band == 0 || id.band == p.n_bands - 1;
   };
   // Slab step, fused peer stores: once an edge tile's outputs are stored, the
-  // publisher warp copies its rows (2D) / planes (3D) u < peer_rows into the
-  // up neighbour's halo (row u + peer_row[0]) and u >= row_hi - peer_rows into
-  // the down neighbour's (u + peer_row[1]) -- peer-memory stores from inside
-  // the step kernel, tile by tile, while the interior is still computing.
-  // Only interior x is copied: the neighbours' x-halo columns are Dirichlet
-  // constants.  16-byte vectors (x = 0 is 32-byte aligned), scalar tail.
+  // publisher warp copies its edge rows into the neighbours' halos
+  // (peer_copy_tile) -- peer-memory stores from inside the step kernel, tile
+  // by tile, while the interior is still computing.
   auto peer_copy = [&](const TileId& id) {
-    const T* src_base = static_cast<const T*>(p.buf[(id.step + 1) & 1]);
-    const int64_t unit = g.d == 3 ? p.plane : p.pitch;
-    const int64_t xw = min((int64_t)g.tile_x, p.nx - id.x0);  // points of this tile's rows
-    const int64_t nvec = xw / 8;
-    const int rows_y = g.d == 3 ? (int)min((int64_t)g.tile_y, p.ny - id.y0) : 1;
-    const int64_t u0 = g.d == 3 ? id.z0 : id.y0;
-    const int nu = g.d == 3 ? g.tile_z : g.tile_y;
-    for (int k = 0; k < 2; ++k) {
-      if (!p.peer_out[k]) continue;
-      T* dst_base = static_cast<T*>(p.peer_out[k]);
-      for (int du = 0; du < nu; ++du) {
-        const int64_t u = u0 + du;
-        if (u >= p.row_hi) break;
-        if (k == 0 ? u >= p.peer_rows : u < p.row_hi - p.peer_rows) continue;
-        for (int ry = 0; ry < rows_y; ++ry) {
-          const int64_t off = p.origin + (g.d == 3 ? u * p.plane + (id.y0 + ry) * p.pitch : u * p.pitch) + id.x0;
-          const T* src = src_base + off;
-          T* dst = dst_base + off + p.peer_row[k] * unit;
-          for (int64_t v = lane; v < nvec; v += 32)
-            reinterpret_cast<uint4*>(dst)[v] = __ldcg(reinterpret_cast<const uint4*>(src) + v);
-          for (int64_t e = nvec * 8 + lane; e < xw; e += 32)
-            reinterpret_cast<uint16_t*>(dst)[e] = __ldcg(reinterpret_cast<const unsigned short*>(src) + e);
-        }
-      }
-    }
+    const T* src = static_cast<const T*>(p.buf[(id.step + 1) & 1]);
+    if constexpr (L == 8) peer_copy_tile_call<T>(p, src, id.z0, id.y0, id.x0, lane);
+    else peer_copy_tile<T>(p, src, id.z0, id.y0, id.x0, lane);
   };
   auto publisher = [&]() {
     if (p.steps == 1 && !p.chain) {  // the whole warp runs this form
