@@ -2610,6 +2610,24 @@ int spd_run_ex(const spd_plan* plan, const spd_grid_desc* gd, void* buf0, void* 
   const bool chained = !persistent && (flags & SPD_RUN_CHAINED) != 0 && steps > 1 && plan->d >= 2 && !plan->g.cg2;
   const bool forward = (flags & SPD_RUN_FORWARD) != 0;
   const int64_t extent = plan->d == 3 ? gd->nz : (plan->d == 2 ? gd->ny : 1);
+  if (!persistent && !chained) {
+    // Plain per-step launches: the parameters of even and odd steps (buffer
+    // roles and tensor maps) are built once, so the host cost per launch is
+    // the launch itself (small grids are otherwise host-bound: encoding two
+    // tensor maps per step cost more than a 512^2 step).
+    StepParams sp2[2];
+    for (int k = 0; k < 2 && k < steps; ++k) {
+      rc = fill_step_params(plan, gd, k ? buf1 : buf0, k ? buf0 : buf1, 0, extent, 1, sp2[k]);
+      if (rc) return rc;
+    }
+    for (int done = 0; done < steps; ++done) {
+      StepParams& sp = sp2[done & 1];
+      sp.reverse = forward ? 0 : (done & 1);
+      rc = dispatch(plan, sp, (cudaStream_t)stream);
+      if (rc) return rc;
+    }
+    return SPD_OK;
+  }
   unsigned int* chain_counters = nullptr;
   int done = 0;
   while (done < steps) {
