@@ -331,13 +331,24 @@ _STEP_PS_PER_POINT = 0.75
 _LAUNCH_OVERHEAD_PS = 4.7e6
 
 
+def _window_weights(windows: int) -> list:
+    """Relative slab sizes: the first and the last window half the size of
+    the others (their upload / download is the part no step hides), while a
+    full window's upload still fits under the previous window's steps (a
+    copied point costs ~48x a point-step, a window ~100 steps)."""
+    if windows <= 2:
+        return [1] * windows
+    return [1] + [2] * (windows - 2) + [1]
+
+
 def _stream_gain(extent: int, row_points: int, margin: int, steps: int, windows: int) -> float:
     """Modelled time saved (ps) by `windows` streamed windows over the
     whole-grid path: the copies of all but the first upload and the last
     download overlap the steps; every window recomputes its margin rows and
     pays its own launch fill and drain."""
     copies = 2 * extent * row_points * _COPY_PS_PER_POINT
-    saved = copies * (1 - 1 / windows)
+    w = _window_weights(windows)
+    saved = copies - copies / 2 * (w[0] + w[-1]) / sum(w)
     margins = steps * 2 * margin * (windows - 1) * row_points * _STEP_PS_PER_POINT
     launches = steps * (windows - 1) * _LAUNCH_OVERHEAD_PS
     return saved - margins - launches
@@ -349,7 +360,8 @@ def stream_windows(extent: int, band: int, steps: int, r: int, windows: int | No
     (slab_lo, slab_hi, win_lo, win_hi) in interior rows (2D) / planes (3D), or
     [] when streaming does not pay.
 
-    The extent is cut into `windows` band-aligned slabs; window k is slab k
+    The extent is cut into `windows` band-aligned slabs (the first and the
+    last half the size of the others, `_window_weights`); window k is slab k
     widened by the margin M = T*r rounded up to whole tile bands (clipped to
     the grid).  After T steps the rows the window's frozen outer halo has
     contaminated lie within T*r of the window edge, outside the slab, and the
@@ -377,12 +389,18 @@ def stream_windows(extent: int, band: int, steps: int, r: int, windows: int | No
     windows = min(int(windows), units)
     if windows < 2:
         return []
+    w = _window_weights(windows)
+    edges, acc = [0], 0
+    for x in w:
+        acc += x
+        edges.append(units * acc // sum(w))
     out = []
     for k in range(windows):
-        lo = units * k // windows * band
-        hi = min(extent, units * (k + 1) // windows * band)
-        out.append((lo, hi, max(0, lo - margin), min(extent, hi + margin)))
-    return out
+        lo = edges[k] * band
+        hi = min(extent, edges[k + 1] * band)
+        if hi > lo:
+            out.append((lo, hi, max(0, lo - margin), min(extent, hi + margin)))
+    return out if len(out) >= 2 else []
 
 
 _STREAMS = threading.local()
