@@ -93,3 +93,57 @@ def test_light_cone_full_size(name, inner, where):
     print(f"light-cone {name} {where}: max-rel vs fp64 oracle after T={T}: {err:.3e}")
     assert err < TOL_T100, err
     assert not torch.equal(got_crop, crop_in[blk_crop])            # the block did evolve
+
+
+@pytest.mark.timeout(600, method="thread")
+def test_large_grid_64bit_offsets():
+    """A 36864^2 fp16 grid (2.7 GB per buffer: element offsets past 2^31
+    bytes): a block at the far corner after 3 steps equals the same block of a
+    small tile-aligned crop run (light cone), bit for bit."""
+    _, _, d, r, kind, _ = bench.CONFIGS["B9"]
+    kern = bench.make_kernel(kind, d, r)
+    plan = get_plan(kern, sp.Parity.EVEN, "fp16")
+    n, T, h = 36864, 3, r
+    full = DeviceGrid(plan, (n, n), h)
+    gen = torch.Generator(device="cuda").manual_seed(31)
+    dense = (torch.rand((n + 2 * h, n + 2 * h), dtype=torch.float32, device="cuda", generator=gen) * 2 - 1).half()
+    full.load_dense_f64(dense.double())
+    full.run(T)
+    out = full.to_dense_f64()
+    inf = plan.info()
+    ty, tx = inf.tile_y, inf.n_tile * inf.L
+    c0y, c0x = (n - 256) // ty * ty, (n - 1024) // tx * tx       # crop origin (dense index), tile-aligned
+    crop_in = dense[c0y:, c0x:].double().contiguous()
+    cg = DeviceGrid(plan, tuple(s - 2 * h for s in crop_in.shape), h)
+    cg.load_dense_f64(crop_in)
+    cg.run(T)
+    got = cg.to_dense_f64()
+    m = r * T  # rows / columns next to the crop's own halo see its frozen edge
+    assert torch.equal(out[c0y + h + m:, c0x + h + m:], got[h + m:, h + m:])
+    assert not torch.equal(out[c0y + h + m:-h, c0x + h + m:-h], dense[c0y + h + m:-h, c0x + h + m:-h].double())
+
+
+@pytest.mark.timeout(600, method="thread")
+def test_large_3d_grid_64bit_offsets():
+    """1024^3 fp16 (2.2 GB per buffer): the far-corner block after 2 steps
+    equals a tile-aligned crop run, bit for bit."""
+    _, _, d, r, kind, _ = bench.CONFIGS["B27"]
+    kern = bench.make_kernel(kind, d, r)
+    plan = get_plan(kern, sp.Parity.EVEN, "fp16")
+    n, T, h = 1024, 2, r
+    full = DeviceGrid(plan, (n, n, n), h)
+    gen = torch.Generator(device="cuda").manual_seed(33)
+    dense = (torch.rand((n + 2 * h,) * 3, dtype=torch.float32, device="cuda", generator=gen) * 2 - 1).half()
+    full.load_dense_f64(dense.double())
+    full.run(T)
+    out = full.to_dense_f64()
+    inf = plan.info()
+    c = [(n - 40) // inf.tile_z * inf.tile_z, (n - 40) // inf.tile_y * inf.tile_y,
+         (n - 256) // (inf.n_tile * inf.L) * (inf.n_tile * inf.L)]
+    crop_in = dense[c[0]:, c[1]:, c[2]:].double().contiguous()
+    cg = DeviceGrid(plan, tuple(s - 2 * h for s in crop_in.shape), h)
+    cg.load_dense_f64(crop_in)
+    cg.run(T)
+    got = cg.to_dense_f64()
+    m = h + r * T
+    assert torch.equal(out[c[0] + m:, c[1] + m:, c[2] + m:], got[m:, m:, m:])
