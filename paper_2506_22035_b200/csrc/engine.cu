@@ -1132,6 +1132,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           }
         }
       }
+#undef SPD_ITEM_OK
       if constexpr (CG2) asm volatile("fence.proxy.async;" ::: "memory");  // the pair's MMA reads this B half
       else fence_proxy_async_smem();
       __syncwarp();
