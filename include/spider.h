@@ -293,10 +293,12 @@ int spd_halo_unpack(const spd_grid_desc* g, void* buf, int rows, int dir,
  * the up_ / dn_ arguments are the neighbours' mapped buffers, layouts and flag
  * words (NULL buffers at the global boundary).
  * spd_slab_step(t): waits (stream memory op) for the neighbours' step t-1
- * halos, computes the two boundary tile bands, copies the r outermost rows
- * into the neighbours' halo rows and bumps their flags on comm_stream, and
- * computes the interior bands on compute_stream.  The result of step t is in
- * buf[(t+1) % 2]. */
+ * halos, computes the two boundary tile bands first (the kernel's publisher
+ * warp copies each finished edge tile's r outermost rows into the neighbours'
+ * halo rows over peer memory; SPD_SLAB_COPY=1: a copy-engine copy on
+ * comm_stream instead), bumps the neighbours' flags on comm_stream once the
+ * edge bands are done, and computes the interior bands on compute_stream.
+ * The result of step t is in buf[(t+1) % 2]. */
 int spd_ipc_export(const void* ptr, void* handle64, int64_t* offset);
 int spd_ipc_open(const void* handle64, int64_t offset, void** ptr, void** base);
 int spd_ipc_close(void* base);
