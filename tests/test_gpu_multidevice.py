@@ -104,3 +104,18 @@ def test_multidevice_bf16_matches_one_device():
     want, _ = sp.execute(k, g, 3, DeviceConfig(dtype="bf16"))
     got, _ = sp.execute(k, g, 3, DeviceConfig(dtype="bf16", devices=(0, 0)))
     assert np.array_equal(got.data, want.data)
+
+
+@gpu
+@pytest.mark.timeout(300, method="thread")
+@pytest.mark.parametrize("two_launch", ["0", "1"])
+def test_multidevice_long_run_both_slab_forms(monkeypatch, two_launch):
+    """64 steps on 3 slabs: the in-kernel peer copies and the flag protocol
+    stay exact over many exchanges, in both slab launch forms."""
+    monkeypatch.setenv("SPD_SLAB_TWO_LAUNCH", two_launch)
+    k = _kernel(2, 1)
+    g = _grid(2, 1, (1536, 2048), np.float16)
+    monkeypatch.setenv("SPD_STREAM_WINDOWS", "0")
+    want, _ = sp.execute(k, g, 64)
+    got, _ = sp.execute(k, g, 64, DeviceConfig(devices=(0, 0, 0)))
+    assert np.array_equal(got.data, want.data)
