@@ -35,6 +35,7 @@ def _grid(d, r, shape, dtype):
     (2, 1, (128, 512), 2, 5, np.float64),      # quantised on the device, fp64 result
     (3, 1, (48, 24, 256), 3, 3, np.float16),
     (3, 1, (32, 16, 128), 2, 2, np.float32),
+    (2, 4, (200, 1000), 2, 3, np.float16),     # generic radius (L = 10): staged epilogue + peer copies
 ])
 def test_multidevice_execute_matches_one_device(d, r, shape, n, steps, dtype):
     k = _kernel(d, r)
