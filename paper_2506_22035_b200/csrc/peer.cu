@@ -231,14 +231,14 @@ int spd_slab_step(spd_slab* s, int t, void* compute_stream, void* comm_stream) {
   // edge tiles); an edge launch + an interior launch costs B9 +8.3 %, W
   // +3.1 %, B27 +3.8 %.  So: two launches for 3D and for large slabs, one
   // launch for small 2D slabs.  SPD_SLAB_TWO_LAUNCH=0/1 overrides.
-  static const char* two_env = getenv("SPD_SLAB_TWO_LAUNCH");
+  const char* two_env = getenv("SPD_SLAB_TWO_LAUNCH");  // read per step: tests switch it in-process
   const bool two_launch = two_env ? atoi(two_env) != 0
                                   : (s->g.dims == 3 || (int64_t)s->per_band * s->n_bands >= 10000);
   // Fused peer stores: the edge tiles' epilogue writes the r outermost rows
   // straight into the neighbours' halo rows (NVLink stores; same layout), so
   // the comm stream only signals -- no copy.  Geometries without them (the
   // generic radii) keep the copy-engine exchange.  SPD_SLAB_COPY=1 forces it.
-  static const char* copy_env = getenv("SPD_SLAB_COPY");
+  const char* copy_env = getenv("SPD_SLAB_COPY");
   const bool fused = plan_peer_stores(s->plan) && !(copy_env && atoi(copy_env) != 0);
   PeerStores ps;
   ps.out[0] = s->has_up ? s->up_buf[(t + 1) & 1] : nullptr;
