@@ -144,7 +144,9 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": max(self.maxsm), "reasons": sorted(self.reasons),
                 "samples": len(self.sm), "source": "nvml",
                 "power_w": round(statistics.median(self.power), 1) if self.power else None,
-                "power_limit_w": self.limit, "reason_bits": hex(self.bits)}
+                "power_limit_w": self.limit, "reason_bits": hex(self.bits),
+                "power_note": "NVML board power, averaged over ~1 s: lags timed regions shorter than that "
+                              "(sustained stepping sits at the limit, profiles/r02_power.txt)"}
 
 
 def measured_peaks():
