@@ -634,7 +634,7 @@ __device__ __noinline__ void peer_copy_tile_call(const StepParams& p, const T* s
 //   producers --(b_full)--> MMA --(b_empty: tcgen05.commit)--> producers
 //   MMA --(acc_full: tcgen05.commit)--> epilogue --(acc_empty)--> MMA
 template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0,
-          bool CG2 = false, int PW = kProdWarpsDefault>
+          bool CG2 = false, int PW = kProdWarpsDefault, bool EDGE = false>
 __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(const __grid_constant__ StepParams p) {
   using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
   constexpr int kProdWarps = C::kProdWarps;
@@ -779,7 +779,13 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
   auto decode_e = [&](int gi, int2 e) {
     TileId id;
     int t;
-    if (!ordered) {
+    if (EDGE) {
+      // slab-step instantiation (edge_order set): plain decode, then the band
+      // index mapped to the edge-first order -- no extra division
+      id.step = 0;
+      id.dep_step = 0;
+      t = gi;
+    } else if (!ordered) {
       id.step = 0;
       id.dep_step = p.chain_t;
       if (p.edge_order) {
@@ -805,8 +811,14 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     }
     const int bx = t % p.tiles_x;
     const int rest = t / p.tiles_x;
-    const int by = rest % p.tiles_y;
-    const int bz = rest / p.tiles_y;
+    int by = rest % p.tiles_y;
+    int bz = rest / p.tiles_y;
+    if constexpr (EDGE) {  // band at launch position `slot` (see the edge_order branch above)
+      int& slot = g.d == 3 ? bz : by;
+      const int nb = p.n_bands;
+      slot = p.edge_order == 1 ? (slot == 0 ? 0 : (slot == 1 ? nb - 1 : slot - 1))
+                               : (slot == 0 ? nb - 1 : (slot == 1 ? 0 : nb - slot));
+    }
     id.x0 = (int64_t)bx * g.tile_x;
     id.y0 = (int64_t)(p.tile_y0 + (g.d == 2 ? by * p.band_stride : by)) * g.tile_y;
     id.z0 = (int64_t)(p.tile_z0 + bz * p.band_stride) * g.tile_z;
@@ -1939,11 +1951,15 @@ static int launch_counters(int n, cudaStream_t st, unsigned int** out) {
 }
 
 template <typename T, int L, int PARITY, int NTILE, int NSTAGE, int NNAT, int NACC, int RIN, int MT = 1, int MTR = 0,
-          bool CG2 = false, int PW = kProdWarpsDefault>
+          bool CG2 = false, int PW = kProdWarpsDefault, bool EDGE = false>
 static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream) {
   using C = Cfg<L, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
   if (CG2 != (plan->g.cg2 != 0)) return set_error(SPD_EUNSUPPORTED, "CTA-pair geometry mismatch");
-  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW>;
+  // the EDGE instantiation (2D fast paths) decodes only edge-first one-step
+  // launches; the others take edge_order through their runtime path
+  if (EDGE && !(sp.edge_order != 0 && sp.steps == 1 && !sp.use_order))
+    return set_error(SPD_EUNSUPPORTED, "edge-first instantiation mismatch");
+  auto kern = spider_step_kernel<T, L, PARITY, NTILE, NSTAGE, NNAT, NACC, RIN, MT, MTR, CG2, PW, EDGE>;
   if (plan->g.r_in != RIN) return set_error(SPD_EUNSUPPORTED, "tile geometry mismatch (r_in %d)", plan->g.r_in);
   if ((L == 4 && MT == 1 && !CG2) != (plan->g.lane_map == 1))
     return set_error(SPD_EUNSUPPORTED, "accumulator lane map mismatch (%d)", plan->g.lane_map);
@@ -2015,7 +2031,10 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   //  stages, items per producer warp>; stage counts fill the 227 KB of smem
   // (scan in profiles/r01_tuning.txt).
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 34)
-    return launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, SPD_2D_NACC, 34>(plan, sp, st);
+    return sp.edge_order
+               ? launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, SPD_2D_NACC, 34, 1, 0, false,
+                             kProdWarpsDefault, true>(plan, sp, st)
+               : launch_step<T, 4, PARITY, 128, SPD_2D_NSTAGE, SPD_2D_NNAT, SPD_2D_NACC, 34>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 128 && g.r_in == 32) return launch_step<T, 4, PARITY, 128, 2, 2, 3, 32>(plan, sp, st);
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.m_tiles == 2)
     return launch_step<T, 4, PARITY, 32, SPD_3D_NSTAGE, SPD_3D_NNAT, SPD_3D_NACC, 100, 2, 40, false, SPD_3D_PW>(plan,
@@ -2023,8 +2042,11 @@ static int dispatch_par(const spd_plan* plan, StepParams& sp, cudaStream_t st) {
   if (g.L == 4 && g.n_tile == 32 && g.r_in == 100 && g.cg2)
     return launch_step<T, 4, PARITY, 32, 2, SPD_3D_NNAT, 3, 100, 1, 0, true, SPD_3D_PW>(plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 22)
-    return launch_step<T, 8, PARITY, 64, SPD_L8_NSTAGE, SPD_L8_NNAT, SPD_L8_NACC, 22, 1, 0, false, SPD_L8_PW>(plan, sp,
-                                                                                                            st);
+    return sp.edge_order
+               ? launch_step<T, 8, PARITY, 64, SPD_L8_NSTAGE, SPD_L8_NNAT, SPD_L8_NACC, 22, 1, 0, false, SPD_L8_PW,
+                             true>(plan, sp, st)
+               : launch_step<T, 8, PARITY, 64, SPD_L8_NSTAGE, SPD_L8_NNAT, SPD_L8_NACC, 22, 1, 0, false, SPD_L8_PW>(
+                     plan, sp, st);
   if (g.L == 8 && g.n_tile == 64 && g.r_in == 16)
     return launch_step<T, 8, PARITY, 64, 3, 4, 4, 16, 1, 0, false, SPD_L8_PW>(plan, sp, st);
   // generic radii (2D: r_in = 128/L + 2r; 1D: r_in = 128/L)
