@@ -73,6 +73,7 @@ SIGNATURES = {
     "spd_plan_operands": (_I, [_P, _U16, _U32, _I32]),
     "spd_plan_geometry": (_I, [_P, _I32, _I32]),
     "spd_plan_lane_map": (_I, [_P, _I32]),
+    "spd_plan_mma_halves": (_I, [_P, _I32]),
     "spd_grid_layout": (_I, [_P, _I64, _I64, _I64, _I, _DESC]),
     "spd_run": (_I, [_P, _DESC, _P, _P, _I, _P]),
     "spd_run_ex": (_I, [_P, _DESC, _P, _P, _I, _I, _P]),

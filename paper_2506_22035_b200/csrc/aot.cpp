@@ -200,6 +200,8 @@ int transform_row(int r, int parity, const double* row, double* values, uint8_t*
 // the same TMEM accumulator (the reference accumulates kernel rows in
 // ascending order, pipeline.py:249-253; here the order is fixed by the MMA
 // sequence and fp32 accumulation).
+static void assign_mma_halves(Geometry* g);
+
 int build_geometry(int d, int r, int flags, Geometry* g) {
   std::memset(g, 0, sizeof(*g));
   int L = band_rows(r);
@@ -322,14 +324,21 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   }
   g->s = s;
   if (s > SPD_MAX_S) return set_error(SPD_EINVAL, "tile needs %d MMAs (max %d)", s, SPD_MAX_S);
+  if (!g->cg2 && !(flags & SPD_PLAN_M128)) assign_mma_halves(g);
   return SPD_OK;
 }
 
 // MMA row (= accumulator TMEM lane) holding output row a, chunk position i.
 int lane_of(const Geometry& g, int a, int i) {
-  if (g.lane_map == 1) {  // 16-lane slabs of 16/L rows; lanes m, m+8 hold positions i, i+1
+  if (g.lane_map == 1) {
+    // 16-lane slabs of 16/L rows; lanes m, m+8 hold positions i, i+1.  Slab
+    // j sits at lane 32 (j % 4) + 16 (j / 4): the top half of the tile's rows
+    // on lanes 0-15 of the four quadrants, the bottom half on lanes 16-31, so
+    // a K-block feeding only one half of the rows is an M = 64 MMA
+    // (assign_mma_halves).
     const int rows16 = 16 / g.L;
-    return 16 * (a / rows16) + (g.L / 2) * (a % rows16) + (i >> 1) + 8 * (i & 1);
+    const int j = a / rows16;
+    return 32 * (j % 4) + 16 * (j / 4) + (g.L / 2) * (a % rows16) + (i >> 1) + 8 * (i & 1);
   }
   return g.L * a + i;
 }
@@ -347,6 +356,29 @@ static int kernel_row_index(const Geometry& g, int b, int a) {
   if (rz < -r || rz > r || ry < -r || ry > r) return -1;
   if (g.d == 2) return rz == 0 ? ry + r : -1;
   return (rz + r) * (2 * r + 1) + (ry + r);
+}
+
+// Which half of the accumulator lanes each MMA feeds (Geometry::mma_half).
+// An M = 64 tcgen05.mma.sp at TMEM lane offset h (D, A and E addresses)
+// computes the rows on lanes 32q + h + [0, 16) of every quadrant q from the
+// same A/E images as the M = 128 form (tools/umma_m64_probe.cu), so an MMA
+// whose input rows feed only output rows on one half can skip the other half:
+// the skipped rows have zero coefficients for those input rows.  MMA 0 stays
+// M = 128: it initialises every accumulator lane (accumulate = 0).
+static void assign_mma_halves(Geometry* g) {
+  const int ranks_rows = g->r_out;  // M-tile 0; the other M-tiles reuse its schedule and images
+  for (int s = 0; s < g->s; ++s) {
+    int used[2] = {0, 0};
+    for (int c = 0; c < g->rows_per_mma; ++c) {
+      const int b = g->start_row[s] + c;
+      if (b < g->first_owned[s]) continue;
+      for (int a = 0; a < ranks_rows; ++a) {
+        if (kernel_row_index(*g, b, a) < 0) continue;
+        for (int i = 0; i < g->L; ++i) used[(lane_of(*g, a, i) % 32) >= 16] = 1;
+      }
+    }
+    g->mma_half[s] = (s == 0 || (used[0] && used[1])) ? 0 : (used[0] ? 1 : (used[1] ? 2 : 0));
+  }
 }
 
 // Packs A (compressed values, logical (s, m, k') order, fp16 or bf16 bits) and

@@ -1278,6 +1278,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     // RIN-RPM), aot.cpp build_geometry).
     const uint32_t idesc = idesc_sparse_f16(CG2 ? 256 : 128, CG2 ? 2 * NTILE : NTILE,
                                             std::is_same<T, __nv_bfloat16>::value);
+    const uint32_t idesc64 = idesc_sparse_f16(64, NTILE, std::is_same<T, __nv_bfloat16>::value);
     constexpr int RPM = 4 / KC;
     constexpr int RIN_MMA = C::RIN_MMA;
     constexpr int S_CT = (RIN_MMA + RPM - 1) / RPM;
@@ -1303,11 +1304,16 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           // descriptor start address field is addr >> 4
           const uint64_t bdesc = bdesc0 + (uint64_t)((start * KC * 128) >> 4);
           if (SPD_DBG_BIT(8)) continue;  // role elimination (SPD_DEVEL builds only)
-          if constexpr (CG2)
+          if constexpr (CG2) {
             mma_sp_ts_elect_cg2(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
-          else
-            mma_sp_ts_elect(dcol + mt * NTILE, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc,
-                            s > 0 ? 1u : 0u);
+          } else {
+            // g.mma_half[s] (aot.cpp assign_mma_halves): 0 -> M = 128; 1 / 2 -> M = 64 on TMEM lanes
+            // 32q + [0, 16) / [16, 32), the same lane offset on D, A and E
+            const int half = g.mma_half[s];
+            const uint32_t loff = half == 2 ? (16u << 16) : 0u;
+            mma_sp_ts_elect(dcol + mt * NTILE + loff, tmem + C::A_COL + 8 * s + loff, bdesc,
+                            tmem + C::E_COL + 2 * s + loff, half ? idesc64 : idesc, s > 0 ? 1u : 0u);
+          }
         }
       }
       if constexpr (CG2) {  // both CTAs' B stage and accumulator barriers
@@ -1430,9 +1436,10 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
      }
     } else if constexpr (C::CPL == 2 && MT == 1 && !CG2) {
     // L = 4, quad-pair lane map (aot.cpp lane_of): accumulator lane
-    // 16 s + 2 rho + (i >> 1) + 8 (i & 1) holds output row 4 s + rho, chunk
-    // position i.  Warp `quad` drains the 16-lane slabs s = 2 quad + h
-    // (h = 0, 1) with tcgen05.ld.16x256b: thread t gets lanes 16 s + t/4
+    // 32 (s % 4) + 16 (s / 4) + 2 rho + (i >> 1) + 8 (i & 1) holds output row
+    // 4 s + rho, chunk position i.  Warp `quad` drains the 16-lane slabs
+    // s = quad + 4 h at lane 32 quad + 16 h (h = 0, 1) with
+    // tcgen05.ld.16x256b: thread t gets lanes 32 quad + 16 h + t/4
     // (position 2 hi, hi = bit 2 of t) and + 8 (position 2 hi + 1), i.e. one
     // packed word of two consecutive x per chunk, for columns 8k + 2 (t & 3)
     // + {0, 1}.  Under the sigma column order the four columns of a 16-column
@@ -1455,7 +1462,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int a = 4 * (2 * quad + h) + rho + (mt + (int)crank) * C::R_OUT;
+        const int a = 4 * (quad + 4 * h) + rho + (mt + (int)crank) * C::R_OUT;  // slab quad + 4 h
         odz[mt][h] = g.out_dz[a];
         ody[mt][h] = g.out_dy[a];
         odx[mt][h] = g.out_dx[a];
@@ -2318,7 +2325,7 @@ int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype
                        spd_plan** out) {
   using namespace spd;
   if (!out) return set_error(SPD_EINVAL, "null output pointer");
-  if (flags & ~(SPD_PLAN_CTA_PAIR | SPD_PLAN_NO_EMBED)) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
+  if (flags & ~(SPD_PLAN_CTA_PAIR | SPD_PLAN_NO_EMBED | SPD_PLAN_M128)) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
   if ((flags & SPD_PLAN_CTA_PAIR) && d != 3) return set_error(SPD_EUNSUPPORTED, "CTA-pair plans are 3D only");
   *out = nullptr;
   if (d < 1 || d > 3) return set_error(SPD_EINVAL, "unsupported dimensionality %d", d);
@@ -2439,6 +2446,12 @@ int spd_plan_lane_map(const spd_plan* plan, int32_t* lane) {
   const spd::Geometry& g = plan->g;
   for (int a = 0; a < g.r_out; ++a)
     for (int i = 0; i < g.L; ++i) lane[g.L * a + i] = spd::lane_of(g, a, i);
+  return SPD_OK;
+}
+
+int spd_plan_mma_halves(const spd_plan* plan, int32_t* half) {
+  if (!plan || !half) return spd::set_error(SPD_EINVAL, "null argument");
+  for (int s = 0; s < plan->g.s; ++s) half[s] = plan->g.mma_half[s];
   return SPD_OK;
 }
 

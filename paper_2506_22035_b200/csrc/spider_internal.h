@@ -53,6 +53,9 @@ struct Geometry {
   int b_sbo;         // bytes between 8-chunk core-matrix groups of the B image
   int start_row[SPD_MAX_S];
   int first_owned[SPD_MAX_S];
+  int mma_half[SPD_MAX_S];  // accumulator lanes MMA s feeds: 0 all 128 (M = 128); 1 / 2 only lanes
+                            // 32q + [0, 16) / 32q + [16, 32) of each quadrant q: issued as an M = 64
+                            // MMA at TMEM lane offset 0 / 16 (D, A and E alike; tools/umma_m64_probe.cu)
   int in_dz[SPD_MAX_RIN], in_dy[SPD_MAX_RIN], in_dx[SPD_MAX_RIN];
   int out_dz[SPD_MAX_ROUT], out_dy[SPD_MAX_ROUT], out_dx[SPD_MAX_ROUT];
 };

@@ -65,12 +65,20 @@ def tile_model(plan, dense, halo):
     # M-tile t runs the same MMA schedule (same A/E) on B rows shifted by
     # t * mt_rows and produces output rows t * r_out ..
     # CTA-pair mode: rank t runs every K-block with its own A images
+    # An M = 64 MMA (half 1 / 2) only writes lanes 0-15 / 16-31 of each
+    # quadrant: the model drops its rows on the other lanes, so a wrong half
+    # assignment loses coefficients and breaks the comparison with the oracle.
+    halves = plan.mma_halves()
+    lane_half = np.where(np.arange(128) % 32 < 16, 1, 2)
     for t in range(2 if inf.cg2 else inf.m_tiles):
         D = np.zeros((128, n_tile))
         for s in range(inf.mmas_per_tile):
             b0 = starts[s] + (0 if inf.cg2 else t * inf.mt_rows)
             Bs = Bimg[b0 : b0 + rpm].transpose(0, 2, 1).reshape(32, n_tile)
-            D += A[t * inf.mmas_per_tile + s if inf.cg2 else s] @ Bs
+            As = A[t * inf.mmas_per_tile + s if inf.cg2 else s]
+            if halves[s]:
+                As = np.where((lane_half == halves[s])[:, None], As, 0.0)
+            D += As @ Bs
         for a in range(inf.r_out):
             dz, dy, dx = out_off[a + t * inf.r_out]
             for i in range(L):
@@ -167,8 +175,10 @@ def test_unsupported_radius_rejected_by_device_plan():
 
 def test_lane_map_is_a_permutation():
     """L = 4 one-M-tile plans (2D, 1D) put output row a, chunk position i on
-    accumulator lane 16*(a/4) + 2*(a%4) + (i>>1) + 8*(i&1) (the epilogue's
-    tcgen05.ld.16x256b order); 3D and other radii keep m = L*a + i."""
+    accumulator lane 32*(j%4) + 16*(j/4) + 2*(a%4) + (i>>1) + 8*(i&1), j = a/4
+    (the epilogue's tcgen05.ld.16x256b order; rows 0-15 on lanes 0-15 of the
+    quadrants, rows 16-31 on lanes 16-31); 3D and other radii keep
+    m = L*a + i."""
     for d, r in ((2, 1), (3, 1), (1, 1), (2, 3), (2, 2)):
         c = np.ones((2 * r + 1,) * d)
         kern = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
@@ -179,11 +189,10 @@ def test_lane_map_is_a_permutation():
         for a in range(inf.r_out):
             for i in range(inf.L):
                 rows16 = 16 // inf.L
-                pair = 16 * (a // rows16) + (inf.L // 2) * (a % rows16) + (i >> 1) + 8 * (i & 1)
+                j = a // rows16
+                pair = 32 * (j % 4) + 16 * (j // 4) + (inf.L // 2) * (a % rows16) + (i >> 1) + 8 * (i & 1)
                 if inf.L == 4 and inf.m_tiles == 1 and not inf.cg2:
                     assert lanes[inf.L * a + i] == pair
-                elif inf.L == 8:  # pair map in SPD_L8_PAIRS builds
-                    assert lanes[inf.L * a + i] in (pair, inf.L * a + i)
                 else:
                     assert lanes[inf.L * a + i] == inf.L * a + i
 
@@ -204,3 +213,30 @@ def test_radius2_embeds_as_radius3():
         finally:
             del os.environ["SPD_NO_EMBED"]
         assert inf.L == 6 and inf.r_dev == 2
+
+
+def test_mma_halves():
+    """K-blocks that feed only one half of the accumulator lanes run as M = 64
+    MMAs (aot.cpp assign_mma_halves): every nonzero A row of such an MMA sits
+    on that half; MMA 0 (accumulate = 0) is always M = 128; SPD_PLAN_M128 and
+    CTA-pair plans issue M = 128 only.  Expected schedules: 2D r = 1 (34 input
+    rows, 4 per MMA) splits at output row 16; 3D r = 1 (y < 4 on lanes 0-15 of
+    each z quadrant) has 5 of 15 half MMAs."""
+    lane_half = np.where(np.arange(128) % 32 < 16, 1, 2)
+    for d, r, want in ((2, 1, [0, 1, 1, 1, 0, 2, 2, 2, 2]), (1, 1, [0, 1, 1, 1, 2, 2, 2, 2]),
+                       (3, 1, [0, 0, 0, 0, 2, 1, 0, 0, 0, 2, 1, 0, 0, 0, 2]), (2, 3, None), (2, 5, None)):
+        c = np.ones((2 * r + 1,) * d)
+        kern = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
+        plan = Plan(kern, "even", "fp16", device=-1)
+        halves = plan.mma_halves()
+        if want is not None:
+            assert list(halves) == want
+        assert halves[0] == 0
+        a_img, _, _ = plan.operands()
+        for s, h in enumerate(halves):
+            if h:
+                nz = np.any(a_img[s] != 0, axis=1)
+                assert np.all(lane_half[nz] == h), (d, r, s)
+        assert not np.any(Plan(kern, "even", "fp16", device=-1, m128=True).mma_halves())
+    k3 = sp.make_kernel_3d("box", 1, np.ones(27))
+    assert not np.any(Plan(k3, "even", "fp16", device=-1, cta_pair=True).mma_halves())
