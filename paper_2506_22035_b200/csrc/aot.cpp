@@ -306,6 +306,10 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   // (The same layout for L = 8 -- 16x256b reads plus a two-level butterfly
   // over lanes ^4, ^8 -- measured B49 97.4 -> 108.0 us: not used.)
   g->lane_map = (L == 4 && g->m_tiles == 1 && !g->cg2) ? 1 : 0;
+  // 3D two-M-tile geometry: z-split lane map (lane_of), so the K-blocks of
+  // the first / last two input planes are M = 64 MMAs (9 of 15 instead of 5
+  // with the linear map's y split).
+  if (d == 3 && g->m_tiles == 2 && !g->cg2) g->lane_map = 2;
   // B image: core matrices (8 chunks x 16 B) of consecutive window K-chunks
   // are adjacent (LBO = 128 B); 8-chunk groups are SBO apart.  UMMA needs the
   // core matrices 128-B aligned, so SBO is a multiple of 128.
@@ -339,6 +343,13 @@ int lane_of(const Geometry& g, int a, int i) {
     const int rows16 = 16 / g.L;
     const int j = a / rows16;
     return 32 * (j % 4) + 16 * (j / 4) + (g.L / 2) * (a % rows16) + (i >> 1) + 8 * (i & 1);
+  }
+  if (g.lane_map == 2) {
+    // 3D M-tile of 4 z-planes x 8 rows (a = 8 z + y), L = 4: quadrant y / 2,
+    // z-planes 0-1 on lanes 0-15 and 2-3 on lanes 16-31 of the quadrant,
+    // 4-lane group 2 (z % 2) + y % 2 inside the half (the epilogue inverts it)
+    const int z = a / 8, y = a % 8;
+    return 32 * (y / 2) + 16 * (z / 2) + 4 * (2 * (z % 2) + (y % 2)) + i;
   }
   return g.L * a + i;
 }

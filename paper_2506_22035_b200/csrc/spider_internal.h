@@ -45,7 +45,8 @@ struct Geometry {
                      // CTA rank t holds output rows t*r_out.. (its own A/E images) and x-half t of B
   int lane_map;      // MMA row (TMEM lane) of output row a, chunk position i: 0 linear (m = L*a + i);
                      // 1 quad pair (L = 4, one M-tile): m = 16*(a/4) + 2*(a%4) + (i>>1) + 8*(i&1), read back
-                     // with tcgen05.ld.16x256b (lanes m and m+8 land in one thread: phases i, i+1)
+                     // with tcgen05.ld.16x256b (lanes m and m+8 land in one thread: phases i, i+1);
+                     // 2 z-split (3D, two M-tiles): m = 32*(y/2) + 16*(z/2) + 4*(2*(z%2) + y%2) + i
   int r_in;          // input image rows per tile
   int s;             // MMAs per tile
   int n_tile;        // x-chunks per tile (MMA N)
