@@ -310,6 +310,9 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   // the first / last two input planes are M = 64 MMAs (9 of 15 instead of 5
   // with the linear map's y split).
   if (d == 3 && g->m_tiles == 2 && !g->cg2) g->lane_map = 2;
+  // L = 8 (r = 3 and embedded r = 2; 2D and 1D): rows 0-7 on lanes 0-15 and
+  // rows 8-15 on lanes 16-31 of the quadrants (B49: 7 of 11 MMAs at M = 64)
+  if (L == 8 && d != 3) g->lane_map = 3;
   // B image: core matrices (8 chunks x 16 B) of consecutive window K-chunks
   // are adjacent (LBO = 128 B); 8-chunk groups are SBO apart.  UMMA needs the
   // core matrices 128-B aligned, so SBO is a multiple of 128.
@@ -351,6 +354,8 @@ int lane_of(const Geometry& g, int a, int i) {
     const int z = a / 8, y = a % 8;
     return 32 * (y / 2) + 16 * (z / 2) + 4 * (2 * (z % 2) + (y % 2)) + i;
   }
+  if (g.lane_map == 3)  // L = 8: quadrant (a % 8) / 2, half a / 8, 8-lane group a % 2
+    return 32 * ((a % 8) / 2) + 16 * (a / 8) + 8 * (a % 2) + i;
   return g.L * a + i;
 }
 

@@ -1574,8 +1574,11 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     const int grp = warp / 4;        // epilogue group: tiles it == grp (mod kEpiGroups)
     const int m = quad * 32 + lane;  // TMEM lane == M row
     // output row of the tile: m / L, or the inverse of the 3D z-split map (aot.cpp lane_of:
-    // quadrant y / 2, half z / 2, 4-lane group 2 (z % 2) + y % 2)
-    const int alpha = g.lane_map == 2 ? 8 * (2 * ((m % 32) / 16) + (m % 16) / 8) + 2 * quad + (m % 8) / 4 : m / L;
+    // quadrant y / 2, half z / 2, 4-lane group 2 (z % 2) + y % 2) or of the
+    // L = 8 half split: quadrant (a % 8) / 2, half a / 8, 8-lane group a % 2)
+    const int alpha = g.lane_map == 2   ? 8 * (2 * ((m % 32) / 16) + (m % 16) / 8) + 2 * quad + (m % 8) / 4
+                      : g.lane_map == 3 ? 8 * ((m % 32) / 16) + 2 * quad + (m % 16) / 8
+                                        : m / L;
     const int d = lane % L;          // position in the L-lane group
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     // output row of this lane in each M-tile (M-tile t holds rows alpha + t*R_OUT)

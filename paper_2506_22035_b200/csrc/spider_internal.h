@@ -47,6 +47,7 @@ struct Geometry {
                      // 1 quad pair (L = 4, one M-tile): m = 16*(a/4) + 2*(a%4) + (i>>1) + 8*(i&1), read back
                      // with tcgen05.ld.16x256b (lanes m and m+8 land in one thread: phases i, i+1);
                      // 2 z-split (3D, two M-tiles): m = 32*(y/2) + 16*(z/2) + 4*(2*(z%2) + y%2) + i
+                     // 3 half split (L = 8): m = 32*((a%8)/2) + 16*(a/8) + 8*(a%2) + i
   int r_in;          // input image rows per tile
   int s;             // MMAs per tile
   int n_tile;        // x-chunks per tile (MMA N)

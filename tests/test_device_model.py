@@ -193,6 +193,8 @@ def test_lane_map_is_a_permutation():
                 pair = 32 * (j % 4) + 16 * (j // 4) + (inf.L // 2) * (a % rows16) + (i >> 1) + 8 * (i & 1)
                 if inf.L == 4 and inf.m_tiles == 1 and not inf.cg2:
                     assert lanes[inf.L * a + i] == pair
+                elif inf.L == 8:
+                    assert lanes[inf.L * a + i] == 32 * ((a % 8) // 2) + 16 * (a // 8) + 8 * (a % 2) + i
                 elif d == 3:
                     z, y = a // 8, a % 8
                     assert lanes[inf.L * a + i] == 32 * (y // 2) + 16 * (z // 2) + 4 * (2 * (z % 2) + y % 2) + i
@@ -227,7 +229,9 @@ def test_mma_halves():
     0-15 of each quadrant, 2-3 on lanes 16-31) has 9 of 15 half MMAs."""
     lane_half = np.where(np.arange(128) % 32 < 16, 1, 2)
     for d, r, want in ((2, 1, [0, 1, 1, 1, 0, 2, 2, 2, 2]), (1, 1, [0, 1, 1, 1, 2, 2, 2, 2]),
-                       (3, 1, [0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 2, 2, 2, 2, 2]), (2, 3, None), (2, 5, None)):
+                       (3, 1, [0, 1, 1, 1, 1, 0, 0, 0, 0, 0, 2, 2, 2, 2, 2]),
+                       (2, 3, [0, 1, 1, 1, 0, 0, 0, 2, 2, 2, 2]), (1, 3, [0, 1, 1, 1, 2, 2, 2, 2]),
+                       (2, 2, [0, 1, 1, 1, 0, 0, 0, 2, 2, 2, 2]), (2, 5, None)):
         c = np.ones((2 * r + 1,) * d)
         kern = sp.make_kernel_3d("box", r, c) if d == 3 else sp.make_kernel("box", d, r, c)
         plan = Plan(kern, "even", "fp16", device=-1)
