@@ -118,13 +118,6 @@ int spd_plan_create(int d, int r, int parity, const double* coeffs, int dtype,
  * path (by default it runs as radius 3 with a zero ring, on the L = 8 fast
  * path). */
 #define SPD_PLAN_NO_EMBED 2
-/* SPD_PLAN_M128: issue every MMA at M = 128.  By default a K-block whose
- * coefficients reach only one half of the accumulator lanes (lanes 0-15 or
- * 16-31 of every 32-lane quadrant) is issued as an M = 64 MMA on that half:
- * same results (the skipped rows multiply zero coefficients), about a third
- * less tensor-core energy per such MMA.  The flag keeps the all-M = 128
- * schedule for comparison. */
-#define SPD_PLAN_M128 4
 int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype,
                        int device, int flags, spd_plan** out);
 int spd_plan_destroy(spd_plan* plan);
@@ -156,8 +149,8 @@ int spd_plan_lane_map(const spd_plan* plan, int32_t* lane);
 /* Accumulator lanes each MMA of the tile schedule feeds (half[s], s <
  * mmas_per_tile): 0 all 128 lanes (an M = 128 MMA); 1 / 2 only lanes 0-15 /
  * 16-31 of each 32-lane quadrant (an M = 64 MMA at that TMEM lane offset;
- * every coefficient of MMA s on the other lanes is zero).  All zero under
- * SPD_PLAN_M128 and in CTA-pair plans. */
+ * every coefficient of MMA s on the other lanes is zero).  All zero in
+ * CTA-pair plans. */
 int spd_plan_mma_halves(const spd_plan* plan, int32_t* half);
 
 /* ---------------------------------------------------------------------------

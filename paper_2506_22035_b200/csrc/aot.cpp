@@ -331,7 +331,9 @@ int build_geometry(int d, int r, int flags, Geometry* g) {
   }
   g->s = s;
   if (s > SPD_MAX_S) return set_error(SPD_EINVAL, "tile needs %d MMAs (max %d)", s, SPD_MAX_S);
-  if (!g->cg2 && !(flags & SPD_PLAN_M128)) assign_mma_halves(g);
+#ifndef SPD_NO_M64  // comparison builds (tools/build_variant.sh -DSPD_NO_M64): every MMA at M = 128
+  if (!g->cg2) assign_mma_halves(g);
+#endif
   return SPD_OK;
 }
 

@@ -504,6 +504,66 @@ struct Cfg : Roles<PW> {
   static constexpr int NQ = (N_ITEMS + PW - 1) / PW;
 };
 
+// Compile-time twin of aot.cpp assign_mma_halves / lane_of for an
+// instantiation: which half of the accumulator lanes MMA s feeds (0: all,
+// M = 128; 1 / 2: lanes 0-15 / 16-31 of every quadrant, M = 64).  The MMA
+// issuer is on B27's critical path (30 N = 32 MMAs per tile), so the choice is
+// folded into its unrolled schedule instead of read per MMA; the launcher
+// checks the table against the plan's.  Tile shapes: MT = 2 -> 3D 8z x 8y
+// (a = 8z + y per M-tile, input row b = 10 iz + iy); RIN = R_OUT -> 1D
+// segments; else 2D rows (input row b feeds output rows b - 2r .. b).
+template <class C, int L, int RIN, int MT>
+__host__ __device__ constexpr int ct_lane_of(int a, int i) {
+  if (MT == 2) {
+    const int z = a / 8, y = a % 8;
+    return 32 * (y / 2) + 16 * (z / 2) + 4 * (2 * (z % 2) + (y % 2)) + i;
+  }
+  if (L == 4) {
+    const int j = a / 4;
+    return 32 * (j % 4) + 16 * (j / 4) + 2 * (a % 4) + (i >> 1) + 8 * (i & 1);
+  }
+  if (L == 8) return 32 * ((a % 8) / 2) + 16 * (a / 8) + 8 * (a % 2) + i;
+  return L * a + i;
+}
+template <class C, int L, int RIN, int MT>
+__host__ __device__ constexpr bool ct_feeds(int b, int a) {
+  if (MT == 2) {
+    const int dz = b / 10 - 1 - a / 8, dy = b % 10 - 1 - a % 8;
+    return dz >= -1 && dz <= 1 && dy >= -1 && dy <= 1;
+  }
+  if (RIN == C::R_OUT) return a == b;  // 1D
+  return b - a >= 0 && b - a <= L - 2;  // 2D: kernel rows rho = b - a - r, r = (L - 2) / 2
+}
+template <class C, int L, int RIN, int MT>
+__host__ __device__ constexpr int ct_mma_half(int s) {
+#ifdef SPD_NO_M64
+  return 0 * s;
+#else
+  constexpr int RPM = 4 / C::KC;
+  constexpr int RM = C::RIN_MMA;
+  if (s == 0) return 0;
+  const int start = s * RPM + RPM <= RM ? s * RPM : RM - RPM;
+  bool used0 = false, used1 = false;
+  for (int b = s * RPM; b < start + RPM; ++b)
+    for (int a = 0; a < C::R_OUT; ++a)
+      if (ct_feeds<C, L, RIN, MT>(b, a))
+        for (int i = 0; i < L; ++i) {
+          if (ct_lane_of<C, L, RIN, MT>(a, i) % 32 >= 16) used1 = true;
+          else used0 = true;
+        }
+  return used0 && used1 ? 0 : (used0 ? 1 : (used1 ? 2 : 0));
+#endif
+}
+// all MMAs of the schedule, 2 bits each (evaluated at compile time)
+template <class C, int L, int RIN, int MT>
+__host__ __device__ constexpr uint64_t ct_halves_mask() {
+  constexpr int RPM = 4 / C::KC;
+  constexpr int S = (C::RIN_MMA + RPM - 1) / RPM;
+  uint64_t m = 0;
+  for (int s = 0; s < S && s < 32; ++s) m |= (uint64_t)ct_mma_half<C, L, RIN, MT>(s) << (2 * s);
+  return m;
+}
+
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
@@ -1279,6 +1339,7 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
     const uint32_t idesc = idesc_sparse_f16(CG2 ? 256 : 128, CG2 ? 2 * NTILE : NTILE,
                                             std::is_same<T, __nv_bfloat16>::value);
     const uint32_t idesc64 = idesc_sparse_f16(64, NTILE, std::is_same<T, __nv_bfloat16>::value);
+    constexpr uint64_t kHalves = CG2 ? 0 : ct_halves_mask<C, L, RIN, MT>();
     constexpr int RPM = 4 / KC;
     constexpr int RIN_MMA = C::RIN_MMA;
     constexpr int S_CT = (RIN_MMA + RPM - 1) / RPM;
@@ -1307,9 +1368,9 @@ __global__ void __launch_bounds__(Roles<PW>::kThreads, 1) spider_step_kernel(con
           if constexpr (CG2) {
             mma_sp_ts_elect_cg2(dcol, tmem + C::A_COL + 8 * s, bdesc, tmem + C::E_COL + 2 * s, idesc, s > 0 ? 1u : 0u);
           } else {
-            // g.mma_half[s] (aot.cpp assign_mma_halves): 0 -> M = 128; 1 / 2 -> M = 64 on TMEM lanes
-            // 32q + [0, 16) / [16, 32), the same lane offset on D, A and E
-            const int half = g.mma_half[s];
+            // ct_mma_half (= the plan's g.mma_half, aot.cpp assign_mma_halves): 0 -> M = 128;
+            // 1 / 2 -> M = 64 on TMEM lanes 32q + [0, 16) / [16, 32), the same lane offset on D, A, E
+            const int half = (int)((kHalves >> (2 * s)) & 3);  // folded: the loop is unrolled
             const uint32_t loff = half == 2 ? (16u << 16) : 0u;
             mma_sp_ts_elect(dcol + mt * NTILE + loff, tmem + C::A_COL + 8 * s + loff, bdesc,
                             tmem + C::E_COL + 2 * s + loff, half ? idesc64 : idesc, s > 0 ? 1u : 0u);
@@ -1982,6 +2043,9 @@ static int launch_step(const spd_plan* plan, StepParams& sp, cudaStream_t stream
     if (plan->g.m_tiles != MT || (MT > 1 && plan->g.mt_rows != MTR))
       return set_error(SPD_EUNSUPPORTED, "M-tile geometry mismatch (%d)", plan->g.m_tiles);
     for (int s = 0; s < plan->g.s; ++s)
+      if (!CG2 && plan->g.mma_half[s] != (int)((ct_halves_mask<C, L, RIN, MT>() >> (2 * s)) & 3))
+        return set_error(SPD_EUNSUPPORTED, "M = 64 schedule mismatch (MMA %d)", s);
+    for (int s = 0; s < plan->g.s; ++s)
       if (plan->g.start_row[s] != (s * RPM + RPM <= RM ? s * RPM : RM - RPM))
         return set_error(SPD_EUNSUPPORTED, "MMA start row mismatch (%d)", s);
   }
@@ -2330,7 +2394,7 @@ int spd_plan_create_ex(int d, int r, int parity, const double* coeffs, int dtype
                        spd_plan** out) {
   using namespace spd;
   if (!out) return set_error(SPD_EINVAL, "null output pointer");
-  if (flags & ~(SPD_PLAN_CTA_PAIR | SPD_PLAN_NO_EMBED | SPD_PLAN_M128)) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
+  if (flags & ~(SPD_PLAN_CTA_PAIR | SPD_PLAN_NO_EMBED)) return set_error(SPD_EINVAL, "unknown plan flags 0x%x", flags);
   if ((flags & SPD_PLAN_CTA_PAIR) && d != 3) return set_error(SPD_EUNSUPPORTED, "CTA-pair plans are 3D only");
   *out = nullptr;
   if (d < 1 || d > 3) return set_error(SPD_EINVAL, "unsupported dimensionality %d", d);

@@ -23,7 +23,6 @@ from .transform import Parity
 TORCH_DTYPES = {"fp16": torch.float16, "bf16": torch.bfloat16}
 SPD_PLAN_CTA_PAIR = 1  # include/spider.h
 SPD_PLAN_NO_EMBED = 2
-SPD_PLAN_M128 = 4
 SPD_RUN_PERSISTENT, SPD_RUN_CHAINED, SPD_RUN_FORWARD, SPD_RUN_STEPMAJOR = 1, 2, 4, 8  # include/spider.h
 # default spd_run_ex flags of DeviceGrid.run (one launch per step)
 RUN_FLAGS = 0
@@ -69,7 +68,7 @@ class Plan:
     """
 
     def __init__(self, kernel: StencilKernel, parity=Parity.EVEN, dtype: str = "fp16", device: int | None = None,
-                 cta_pair: bool = False, m128: bool = False):
+                 cta_pair: bool = False):
         if dtype not in DTYPE_CODES:
             raise ValueError(f"dtype must be one of {sorted(DTYPE_CODES)}, got {dtype!r}")
         self.kernel = kernel
@@ -83,8 +82,6 @@ class Plan:
         self.cta_pair = bool(cta_pair)
         h = C.c_void_p()
         flags = SPD_PLAN_CTA_PAIR if cta_pair else 0
-        if m128:  # every MMA at M = 128 (comparison; default issues M = 64 half-lane MMAs)
-            flags |= SPD_PLAN_M128
         if os.environ.get("SPD_NO_EMBED"):  # development override: radius 2 on the generic L = 6 path
             flags |= SPD_PLAN_NO_EMBED
         check(lib.spd_plan_create_ex(kernel.d, kernel.r, self.parity.code, dptr(coeffs), DTYPE_CODES[dtype],

@@ -258,16 +258,19 @@ def _stats(kernel: StencilKernel, grid, steps: int, cfg, plan: Plan) -> ExecStat
         info = plan.info()
         tiles_x = -(-grid.B // (info.n_tile * L)) if kernel.d != 1 else -(-grid.B // (info.n_tile * L * info.r_out))
         tiles = tiles_x * (-(-grid.A // info.tile_y) if kernel.d >= 2 else 1) * (-(-planes // info.tile_z))
+        halves = plan.mma_halves()
+        n64 = int(np.count_nonzero(halves))  # M = 64 half-lane MMAs per M-tile
         st.device = {
             "arch": "sm_100a",
-            "instruction": "tcgen05.mma.sp.cta_group::1.kind::f16 M128 N%d K32" % info.n_tile,
+            "instruction": "tcgen05.mma.sp.cta_group::1.kind::f16 M128|M64 N%d K32" % info.n_tile,
             "dtype": plan.dtype,
             "launches": steps,
             "tiles_per_step": tiles,
             "tile": {"n_tile": info.n_tile, "tile_rows": info.r_out * info.m_tiles, "tile_z": info.tile_z,
                      "input_rows": info.r_in, "mmas_per_tile": info.mmas_per_tile * info.m_tiles},
             "mma_instructions": steps * tiles * info.mmas_per_tile * info.m_tiles,
-            "issued_sparse_macs": steps * tiles * info.mmas_per_tile * info.m_tiles * 128 * info.n_tile * 16,
+            "m64_instructions": steps * tiles * n64 * info.m_tiles,
+            "issued_sparse_macs": steps * tiles * (info.mmas_per_tile * 128 - n64 * 64) * info.m_tiles * info.n_tile * 16,
         }
     return st
 

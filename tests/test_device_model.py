@@ -223,8 +223,8 @@ def test_radius2_embeds_as_radius3():
 def test_mma_halves():
     """K-blocks that feed only one half of the accumulator lanes run as M = 64
     MMAs (aot.cpp assign_mma_halves): every nonzero A row of such an MMA sits
-    on that half; MMA 0 (accumulate = 0) is always M = 128; SPD_PLAN_M128 and
-    CTA-pair plans issue M = 128 only.  Expected schedules: 2D r = 1 (34 input
+    on that half; MMA 0 (accumulate = 0) is always M = 128; CTA-pair plans
+    issue M = 128 only.  Expected schedules: 2D r = 1 (34 input
     rows, 4 per MMA) splits at output row 16; 3D r = 1 (z-planes 0-1 on lanes
     0-15 of each quadrant, 2-3 on lanes 16-31) has 9 of 15 half MMAs."""
     lane_half = np.where(np.arange(128) % 32 < 16, 1, 2)
@@ -244,6 +244,5 @@ def test_mma_halves():
             if h:
                 nz = np.any(a_img[s] != 0, axis=1)
                 assert np.all(lane_half[nz] == h), (d, r, s)
-        assert not np.any(Plan(kern, "even", "fp16", device=-1, m128=True).mma_halves())
     k3 = sp.make_kernel_3d("box", 1, np.ones(27))
     assert not np.any(Plan(k3, "even", "fp16", device=-1, cta_pair=True).mma_halves())

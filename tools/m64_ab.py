@@ -1,7 +1,9 @@
-"""A/B of the M = 64 half-lane MMAs against the all-M = 128 schedule
-(SPD_PLAN_M128): result hash, short-run step time at full clock (after a
-cool-down) and sustained energy / time per step under the board power cap.
-usage: python tools/m64_ab.py [seconds] CONFIG..."""
+"""One arm of an A/B between library builds (SPD_LIB=...; e.g. the all-M = 128
+build of tools/build_variant.sh nom64 -DSPD_NO_M64): result hash, short-run
+step time at full clock (after a cool-down) and sustained energy / time per
+step under the board power cap.
+usage: [SPD_LIB=...] python tools/m64_ab.py [seconds] CONFIG..."""
+import os
 import hashlib
 import sys
 import time
@@ -52,28 +54,24 @@ def sustained(g, T):
     return e0.elapsed_time(e1) * 1e3 / n, mj / n, pynvml.nvmlDeviceGetClockInfo(nv, pynvml.NVML_CLOCK_SM)
 
 
+tag = os.path.basename(os.environ.get("SPD_LIB", "libspider.so"))
 for name in args or ["B9", "B27"]:
     desc, shape, d, r, kind, T = bench.CONFIGS[name]
-    kern = bench.make_kernel(kind, d, r)
-    grids = {}
-    for m128 in (True, False):
-        plan = Plan(kern, sp.Parity.EVEN, "fp16", m128=m128)
-        g = DeviceGrid(plan, shape, r)
-        gen = torch.Generator(device="cuda").manual_seed(7)
-        g.load_dense_f64(torch.rand(g.dense_shape, dtype=torch.float64, device="cuda", generator=gen) - 0.5)
-        g.run(T)
-        torch.cuda.synchronize()
-        h = hashlib.sha1(g.bufs[g.cur].cpu().numpy().tobytes()).hexdigest()[:12]
-        grids[m128] = (plan, g, h)
-        print(f"{name} {'M128' if m128 else 'M64 '} halves={list(plan.mma_halves())} hash={h}", flush=True)
-    print(f"{name}: results bit-identical: {grids[True][2] == grids[False][2]}", flush=True)
-    for rep in range(2):
-        for m128 in (True, False):
-            g = grids[m128][1]
-            us = short(g, T)
-            sus, mj, clk = sustained(g, T)
-            pts = 1
-            for v in shape:
-                pts *= v
-            print(f"{name} {'M128' if m128 else 'M64 '} rep {rep}: short {us:7.2f} us/step ({pts / us / 1e3:7.1f} GStencil/s)"
-                  f" | sustained {sus:7.2f} us/step ({pts / sus / 1e3:7.1f}) {mj:6.1f} mJ/step at {clk} MHz", flush=True)
+    plan = Plan(bench.make_kernel(kind, d, r), sp.Parity.EVEN, "fp16")
+    g = DeviceGrid(plan, shape, r)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    g.load_dense_f64(torch.rand(g.dense_shape, dtype=torch.float64, device="cuda", generator=gen) - 0.5)
+    g.run(T)
+    torch.cuda.synchronize()
+    h = hashlib.sha1(g.bufs[g.cur].cpu().numpy().tobytes()).hexdigest()[:12]
+    try:
+        halves = "".join(str(int(v)) for v in plan.mma_halves())
+    except Exception:  # a library from before spd_plan_mma_halves
+        halves = "-"
+    us = short(g, T)
+    sus, mj, clk = sustained(g, T)
+    pts = 1
+    for v in shape:
+        pts *= v
+    print(f"{name} {tag:22s} halves {halves:16s} hash {h}: short {us:7.2f} us/step ({pts / us / 1e3:7.1f} GStencil/s)"
+          f" | sustained {sus:7.2f} us/step ({pts / sus / 1e3:7.1f}) {mj:6.1f} mJ/step at {clk} MHz", flush=True)
