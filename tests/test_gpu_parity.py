@@ -577,3 +577,19 @@ def test_device_stats_equal_host_counters():
     assert dev.pop("device")["mma_instructions"] > 0
     host.pop("device")
     assert dev == host
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,r,halves_per_tile", [(2, 1, 7), (2, 3, 7), (3, 1, 18), (1, 1, 7)])
+def test_m64_half_lane_mmas_counted_and_exact(d, r, halves_per_tile):
+    """The step schedule issues M = 64 MMAs on one half of the accumulator
+    lanes where a K-block feeds only that half (aot.cpp assign_mma_halves,
+    engine.cu ct_halves_mask); the device block counts them (per M-tile) and
+    the result still matches the oracle."""
+    kern = rand_kernel("box", d, r, seed=50 + d + r)
+    shape = {1: (1, 3000), 2: (70, 600), 3: (12, 10, 200)}[d]  # 1D problems use A = 1
+    got, want, _, stats = run_case(kern, shape, 2)
+    dev = stats.device
+    assert dev["m64_instructions"] == 2 * dev["tiles_per_step"] * halves_per_tile
+    inner = tuple(slice(r, -r) for _ in range(max(d, 2)))
+    assert max_rel_error(got.interior, want[inner]) < TOL["fp16"]
