@@ -1,6 +1,7 @@
 """B27 with the default two-M-tile 3D geometry against SPD_PLAN_3D_MT3 (three
 M-tiles per tile): result hashes (must match) plus short-run and sustained
-time / energy per step, interleaved.  usage: python tools/mt3_ab.py [seconds] [CONFIG]"""
+time / energy per step, interleaved.  usage: python tools/mt3_ab.py [seconds] [CONFIG]
+Needs the experiment build of profiles/r02_mt3.txt (the flag was reverted)."""
 import sys
 import time
 from pathlib import Path
