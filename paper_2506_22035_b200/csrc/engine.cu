@@ -506,10 +506,11 @@ struct Cfg : Roles<PW> {
 
 // Compile-time twin of aot.cpp assign_mma_halves / lane_of for an
 // instantiation: which half of the accumulator lanes MMA s feeds (0: all,
-// M = 128; 1 / 2: lanes 0-15 / 16-31 of every quadrant, M = 64).  The MMA
-// issuer is on B27's critical path (30 N = 32 MMAs per tile), so the choice is
-// folded into its unrolled schedule instead of read per MMA; the launcher
-// checks the table against the plan's.  Tile shapes: MT = 2 -> 3D 8z x 8y
+// M = 128; 1 / 2: lanes 0-15 / 16-31 of every quadrant, M = 64).  The choice
+// is folded into the issuer's unrolled schedule: reading it per MMA from the
+// kernel parameters put constant-bank loads into B27's issue chain (30 N = 32
+// MMAs per tile) and cost 11 % per launch (profiles/r02_m64_ct.txt).  The
+// launcher checks the table against the plan's.  Tile shapes: MT = 2 -> 3D 8z x 8y
 // (a = 8z + y per M-tile, input row b = 10 iz + iy); RIN = R_OUT -> 1D
 // segments; else 2D rows (input row b feeds output rows b - 2r .. b).
 template <class C, int L, int RIN, int MT>
