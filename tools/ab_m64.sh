@@ -1,3 +1,9 @@
+#!/bin/bash
+# One-box A/B of three library builds (profiles/r02_m64_ct.txt):
+#   tools/libspider_old.so   : the sources of commit 4694419 (before the M = 64 MMAs), built with the nvcc
+#                              lines of tools/build_variant.sh from a `git archive 4694419` checkout
+#   tools/libspider_nom64.so : tools/build_variant.sh nom64 -DSPD_NO_M64
+#   the in-tree library
 timeout 300 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
 for rep in 1 2; do
 for lib in tools/libspider_old.so tools/libspider_nom64.so paper_2506_22035_b200/libspider.so; do
